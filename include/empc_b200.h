@@ -1,0 +1,156 @@
+/*
+ * empc_b200.h -- C ABI of the B200-native Evolutionary MPC (EMPC) hot path.
+ *
+ * The reference (knotmpc, pure Python) has no FFI: its boundary is the
+ * Python API of knotmpc/empc.py.  These entry points are what a binding
+ * (ctypes / cffi / pybind) of that API calls; each one cites the reference
+ * function it replaces (paths relative to /root/reference/pkg/src/knotmpc):
+ *
+ *   empc_run      <- solve_empc          empc.py:211-236   (cold/warm solve)
+ *                 <- init_population     empc.py:162-171   (init only)
+ *                 <- evolve_generation   empc.py:174-208   (one generation)
+ *   empc_score    <- _CostModel.__call__ empc.py:147-152   (batch scorer seam)
+ *                 <- evaluate_cost       empc.py:155-159   (N = 1)
+ *   empc_select   <- argsort(kind="stable")[:K] / argmin   empc.py:185-186, 234
+ *   empc_expand   <- expand / input_at   param.py:91-116   (knots -> inputs)
+ *   empc_set_schedule <- KnotSchedule.coeffs / interpolation_matrix param.py:49-111
+ *   empc_set_problems <- MpcSpec + DiscreteLinearModel condense.py:42-87, dynamics.py:223-238
+ *
+ * Conventions: row-major arrays; every pointer argument is a HOST pointer
+ * borrowed for the duration of the call (device buffers are owned by the
+ * handle).  Floating-point inputs/outputs are FP64 like the reference; the
+ * device computes in the precision chosen at creation (FP32 default).
+ * Every function returns 0 on success or a negative EMPC_E* code, with a
+ * message available from empc_last_error().  One handle per host thread;
+ * distinct handles may be used concurrently.
+ */
+#ifndef EMPC_B200_H_
+#define EMPC_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  EMPC_OK = 0,
+  EMPC_EINVAL = -1,   /* invalid argument (Python layer raises ValueError) */
+  EMPC_ECUDA = -2,    /* CUDA runtime error (RuntimeError) */
+  EMPC_ESTATE = -3,   /* call order / missing problem, schedule or population */
+  EMPC_ENOMEM = -4,
+};
+
+enum { EMPC_FP32 = 0, EMPC_FP64 = 1 };
+
+typedef struct empc_handle empc_handle;
+
+/* Problem shape shared by all instances of a handle (EmpcSettings
+ * num_sims / num_parents, empc.py:31-32; MpcSpec dims, condense.py:42-56). */
+typedef struct {
+  int32_t n;           /* state dimension  (model.n) */
+  int32_t m;           /* input dimension  (model.m) */
+  int32_t T;           /* horizon (MpcSpec.T == KnotSchedule.T) */
+  int32_t p;           /* knot count (KnotSchedule.p) */
+  int32_t num_sims;    /* N */
+  int32_t num_parents; /* K, 1 <= K <= N */
+  int32_t instances;   /* independent MPC problems batched in one handle */
+  int32_t dense_q;     /* 0: Q diagonal (empc.py:114-116 fast path), 1: dense Q */
+  int32_t precision;   /* EMPC_FP32 (default) or EMPC_FP64 */
+  int32_t device;      /* CUDA device ordinal */
+} empc_dims;
+
+int empc_create(const empc_dims* dims, empc_handle** out);
+void empc_destroy(empc_handle* h);
+/* Last error message of the handle (or of the last failed empc_create when h is NULL). */
+const char* empc_last_error(const empc_handle* h);
+
+/* Knot schedule: per step k in [0,T): u_k = (1-c_k) U[idx1_k] + c_k U[idx2_k]
+ * (param.py:30-46, p==1 -> idx1=idx2=0, c=0). */
+int empc_set_schedule(empc_handle* h, const int32_t* idx1, const int32_t* idx2, const double* c);
+
+/* Problems of instances [first, first+count).  Per instance, contiguous:
+ * Ad[n*n] Bd[n*m] wd[n] Q[n*n] R[m*m] x_goal[n] u_goal[m] u_min[m] u_max[m]. */
+int empc_set_problems(empc_handle* h, int32_t first, int32_t count, const double* Ad, const double* Bd,
+                      const double* wd, const double* Q, const double* R, const double* x_goal,
+                      const double* u_goal, const double* u_min, const double* u_max);
+
+/* Population slots: device-resident (N x p x m candidates, N costs) per instance. */
+int empc_pop_alloc(empc_handle* h, int32_t* slot);
+int empc_pop_free(empc_handle* h, int32_t slot);
+/* D2H read of a slot (FP64 out; either pointer may be NULL); generation is host-side state. */
+int empc_pop_read(empc_handle* h, int32_t slot, double* cands, double* costs);
+/* H2D write of a slot (e.g. a Population built on the host). costs may be NULL (zeros). */
+int empc_pop_write(empc_handle* h, int32_t slot, const double* cands, const double* costs);
+
+/* Injected random tensors (parity mode) replacing the in-kernel Philox
+ * streams: the reference's draws of empc.py:168-170 / 195-199. */
+typedef struct {
+  const double* init;          /* instances x N x p x m, or NULL */
+  const int32_t* parents;      /* evolves x instances x (N-K) x 2, or NULL */
+  const uint8_t* take_second;  /* evolves x instances x (N-K) x p x m */
+  const uint8_t* mutate;       /* evolves x instances x (N-K) x p x m */
+  const double* noise;         /* evolves x instances x (N-K) x p x m */
+} empc_injected;
+
+typedef struct {
+  int32_t init;             /* 1: cold start (uniform knots, empc.py:168-170) */
+  int32_t rescore;          /* 1: re-score slot_in at x0 before evolving (empc.py:229-231) */
+  int32_t evolves;          /* number of evolve_generation steps */
+  int32_t slot_in;          /* population read when init == 0 (-1 otherwise) */
+  int32_t slot_out;         /* slot receiving the final population (-1: keep internal only) */
+  int64_t generation0;      /* Population.generation at entry (RNG key of the first evolve) */
+  uint64_t seed;            /* EmpcSettings.seed */
+  double mutation_prob;     /* EmpcSettings.mutation_prob */
+  double crossover_prob;    /* EmpcSettings.crossover_prob */
+  const double* x0;         /* instances x n */
+  const double* sigma;      /* instances x m: mutation std of empc.py:73-82 (host-computed, FP64) */
+  const empc_injected* inject; /* NULL: in-kernel counter-based Philox4x32-10 */
+  /* outputs, each may be NULL */
+  double* u_out;            /* instances x m      (EmpcResult.u) */
+  double* best_out;         /* instances x p x m  (EmpcResult.best) */
+  double* best_cost;        /* instances          (EmpcResult.best_cost) */
+  int32_t* best_index;      /* instances          (argmin row) */
+} empc_run_args;
+
+/* Run init / rescore / evolves as one device-resident sequence (graph-captured
+ * when no injection is given).  Synchronous: returns after outputs are on the host. */
+int empc_run(empc_handle* h, const empc_run_args* args);
+
+/* Score `num` candidates per instance at x0 (instances x n) with the rollout
+ * kernel: cands instances x num x p x m -> costs instances x num. */
+int empc_score(empc_handle* h, const double* x0, int32_t num, const double* cands, double* costs);
+
+/* Stable selection on given costs (instances x N): elite_idx instances x K
+ * (= argsort(kind="stable")[:K]) and best_index (= argmin, first NaN wins). */
+int empc_select(empc_handle* h, const double* costs, int32_t* elite_idx, int32_t* best_index);
+
+/* Knot expansion (kernel K1): cands num x p x m -> traj num x T x m. */
+int empc_expand(empc_handle* h, int32_t num, const double* cands, double* traj);
+
+/* Device-resident timing for bench.py: `reps` replays of the run described by
+ * args with inputs already in HBM (no H2D/D2H inside the timed region).
+ * ms_each[reps] receives each replay's CUDA-event time; when flush_l2 != 0 a
+ * buffer larger than L2 is overwritten before each replay (untimed).
+ * rollout_ms (may be NULL) receives the mean duration of one rollout
+ * launch and rollout_launches the number of rollout launches per replay;
+ * launches_per_rep the number of kernels per replay. */
+int empc_time_device(empc_handle* h, const empc_run_args* args, int32_t reps, int32_t flush_l2,
+                     float* ms_each, float* rollout_ms, int32_t* rollout_launches, int32_t* launches_per_rep);
+
+/* Selected rollout variant for diagnostics: writes a short description. */
+int empc_describe(empc_handle* h, char* buf, int32_t len);
+
+/* Rollout kernel variants compiled for this handle's padded state size
+ * (register blocking / A-in-registers choices); -1 restores the heuristic. */
+int empc_num_variants(empc_handle* h, int32_t* count);
+int empc_set_variant(empc_handle* h, int32_t variant);
+
+/* Known-answer seam for the in-kernel counter-based RNG: Philox4x32-10 of
+ * `count` (ctr[4], key[2]) pairs evaluated on the device. */
+int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMPC_B200_H_ */

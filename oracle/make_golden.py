@@ -1,0 +1,150 @@
+"""Generate the golden fixtures under tests/golden/ from the REAL reference.
+
+Run in the build container (where /root/reference exists):
+
+    python oracle/make_golden.py
+
+It imports ``knotmpc`` from /root/reference/pkg/src (read-only) and records
+inputs and outputs of the hot-path functions so that (a) the oracle
+restatement in ``oracle/empc_oracle.py`` can be pinned against the reference
+on any machine, and (b) the GPU parity tests have reference vectors without
+needing /root/reference at run time.  The fixtures are small (.npz).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def _import_ref():
+    sys.path.insert(0, REF)
+    import knotmpc  # noqa: F401
+    from knotmpc import condense, dynamics, empc, param
+    return condense, dynamics, empc, param
+
+
+def spec_arrays(spec, prefix=""):
+    m = spec.model
+    return {
+        prefix + "Ad": m.Ad, prefix + "Bd": m.Bd, prefix + "wd": m.wd, prefix + "T": np.int64(spec.T),
+        prefix + "Q": spec.Q, prefix + "R": spec.R, prefix + "x_goal": spec.x_goal,
+        prefix + "u_goal": spec.u_goal, prefix + "u_min": spec.u_min, prefix + "u_max": spec.u_max,
+    }
+
+
+def main():
+    condense, dynamics, empc, param = _import_ref()
+    os.makedirs(OUT, exist_ok=True)
+
+    # -- knot schedules: W for every config's (T, p) plus the reference's frozen cases
+    wcases = [(5, 3), (7, 7), (8, 1), (20, 2), (20, 3), (50, 3), (50, 4), (200, 5), (23, 6), (15, 4), (11, 4),
+              (120, 7), (100, 34), (99, 50)]
+    wd = {}
+    for T, p in wcases:
+        s = param.KnotSchedule(T=T, p=p)
+        wd[f"W_{T}_{p}"] = param.interpolation_matrix(s)
+        co = np.array([s.coeffs(k) for k in range(T)], dtype=object)
+        wd[f"idx_{T}_{p}"] = np.array([[int(a), int(b)] for a, b, _ in co], np.int64)
+        wd[f"c_{T}_{p}"] = np.array([float(c) for _, _, c in co])
+    np.savez_compressed(os.path.join(OUT, "knots.npz"), **wd)
+
+    # -- the reference test system (TST/test_empc.py:20-36)
+    Ad = np.array([[1.0, 0.02], [-0.4, 0.97]])
+    Bd = np.array([[0.0], [0.05]])
+    model = dynamics.DiscreteLinearModel(Ad, Bd, np.zeros(2), 0.02)
+    spec2 = condense.MpcSpec(model, 20, Q=np.diag([10.0, 0.1]), R=0.01 * np.eye(1),
+                             x_goal=np.array([0.5, 0.0]), u_goal=np.zeros(1),
+                             u_min=-np.array([4.0]), u_max=np.array([4.0]))
+    x02 = np.array([-0.3, 0.1])
+    sched2 = param.KnotSchedule(T=20, p=3)
+
+    # -- n-link systems built with the reference's own recipe
+    def nlink_case(D, T, p, seed):
+        plant = dynamics.NLinkArm(dynamics.NLinkParams(links=D))
+        rng = np.random.default_rng(seed)
+        q0 = rng.uniform(-np.pi, np.pi, D)
+        qg = rng.uniform(-np.pi, np.pi, D)
+        x0 = np.concatenate([q0, np.zeros(D)])
+        xg = np.concatenate([qg, np.zeros(D)])
+        mdl = dynamics.discretize(dynamics.linearize(plant.ode, x0, np.zeros(D)), 0.01)
+        spec = condense.MpcSpec(mdl, T, Q=np.diag([10.0] * D + [0.1] * D), R=0.01 * np.eye(D),
+                                x_goal=xg, u_goal=np.zeros(D), u_min=np.full(D, -2.0), u_max=np.full(D, 2.0))
+        return spec, param.KnotSchedule(T=T, p=p), x0
+
+    cases = {
+        "spec2": (spec2, sched2, x02),
+        "c1": nlink_case(2, 20, 2, 0),
+        "c2": nlink_case(6, 50, 3, 0),
+        "c3s": nlink_case(24, 50, 4, 0),   # C3 system, scored on a small population
+    }
+    # dense-Q / dense-R / drift variant of the 6-DoF system
+    s6, sc6, x6 = cases["c2"]
+    rng = np.random.default_rng(42)
+    Mq = rng.normal(size=(12, 12))
+    Mr = rng.normal(size=(6, 6))
+    dense = condense.MpcSpec(dynamics.DiscreteLinearModel(s6.model.Ad, s6.model.Bd, 0.01 * rng.normal(size=12), 0.01),
+                             50, Q=Mq @ Mq.T / 12, R=Mr @ Mr.T / 6 + 0.1 * np.eye(6), x_goal=s6.x_goal,
+                             u_goal=0.1 * rng.normal(size=6), u_min=s6.u_min, u_max=s6.u_max)
+    cases["dense"] = (dense, sc6, x6)
+
+    for name, (spec, sched, x0) in cases.items():
+        rng = np.random.default_rng(123)
+        N = 64
+        cands = rng.uniform(spec.u_min, spec.u_max, size=(N, sched.p, spec.model.m))
+        cm = empc._CostModel(spec, sched, x0)
+        d = spec_arrays(spec)
+        d.update(p=np.int64(sched.p), x0=x0, cands=cands, cost_condensed=cm(cands),
+                 cost_rollout=empc._rollout_costs(cands, spec, sched, x0),
+                 cost_single=np.array([empc.evaluate_cost(cands[i], spec, sched, x0) for i in range(4)]))
+        np.savez_compressed(os.path.join(OUT, f"score_{name}.npz"), **d)
+
+    # -- full solves (cold and warm) plus the RNG tap for the test system and C1
+    solves = {
+        "spec2_g3": (cases["spec2"], empc.EmpcSettings(num_sims=64, num_parents=8, seed=7, generations=3)),
+        "spec2_p1": ((spec2, param.KnotSchedule(T=20, p=1), x02), empc.EmpcSettings(num_sims=64, num_parents=8, seed=7, generations=2)),
+        "spec2_kn": (cases["spec2"], empc.EmpcSettings(num_sims=8, num_parents=8, seed=7, generations=2)),
+        "c1_g10": (cases["c1"], empc.EmpcSettings(num_sims=100, num_parents=6, seed=1, generations=10)),
+        "c2_g3": (cases["c2"], empc.EmpcSettings(num_sims=1024, num_parents=64, seed=1, generations=3)),
+    }
+    for name, ((spec, sched, x0), st) in solves.items():
+        res = empc.solve_empc(spec, sched, st, x0)
+        warm = empc.solve_empc(spec, sched, st, x0 + 0.01, prev=res.population)
+        d = spec_arrays(spec)
+        d.update(p=np.int64(sched.p), x0=x0, N=np.int64(st.num_sims), K=np.int64(st.num_parents),
+                 G=np.int64(st.generations), seed=np.int64(st.seed),
+                 u=res.u, best=res.best, best_cost=np.float64(res.best_cost),
+                 pop_cands=res.population.candidates, pop_costs=res.population.costs,
+                 pop_gen=np.int64(res.population.generation),
+                 warm_best=warm.best, warm_best_cost=np.float64(warm.best_cost),
+                 warm_pop_cands=warm.population.candidates, warm_pop_costs=warm.population.costs,
+                 warm_gen=np.int64(warm.population.generation))
+        # RNG tap for generation 1 (the first evolve), in the reference's own draw order
+        if st.num_sims > st.num_parents:
+            g = empc._rng(st.seed, 1)
+            nc = st.num_sims - st.num_parents
+            d.update(tap_parents=g.integers(0, st.num_parents, size=(nc, 2)),
+                     tap_take_second=g.random((nc, sched.p, spec.model.m)) < st.crossover_prob,
+                     tap_mutate=g.random((nc, sched.p, spec.model.m)) < st.mutation_prob,
+                     tap_noise=g.normal(size=(nc, sched.p, spec.model.m)))
+            g0 = empc._rng(st.seed, 0)
+            d.update(tap_init=g0.uniform(spec.u_min, spec.u_max, size=(st.num_sims, sched.p, spec.model.m)),
+                     sigma=empc._mutation_sigma(spec, st, x0))
+        np.savez_compressed(os.path.join(OUT, f"solve_{name}.npz"), **d)
+
+    # -- state-bounded spec (rollout scoring path, K/empc.py:138)
+    sb = condense.MpcSpec(spec2.model, 20, spec2.Q, spec2.R, spec2.x_goal, spec2.u_goal, spec2.u_min, spec2.u_max,
+                          x_min=-10.0 * np.ones(2), x_max=10.0 * np.ones(2))
+    pop = empc.init_population(sb, sched2, empc.EmpcSettings(num_sims=64, num_parents=8, seed=7), x02)
+    np.savez_compressed(os.path.join(OUT, "bounded.npz"), cands=pop.candidates, costs=pop.costs)
+
+    print("wrote", sorted(os.listdir(OUT)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+"""ctypes binding of the C ABI in include/empc_b200.h.
+
+The shared library ``libempc_b200.so`` (built in-tree by
+``__graft_entry__.build()`` / ``make -C paper_2001_04931_b200/csrc``) is the
+only compute path: there is no CPU fallback.  Importing this module never
+touches the GPU; the library is loaded on first use and a missing library
+raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libempc_b200.so")
+
+EMPC_OK, EMPC_EINVAL, EMPC_ECUDA, EMPC_ESTATE, EMPC_ENOMEM = 0, -1, -2, -3, -4
+EMPC_FP32, EMPC_FP64 = 0, 1
+
+# every symbol include/empc_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_problems",
+    "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
+    "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
+    "empc_set_variant", "empc_philox",
+)
+
+
+class empc_dims(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in
+                ("n", "m", "T", "p", "num_sims", "num_parents", "instances", "dense_q", "precision", "device")]
+
+
+class empc_injected(C.Structure):
+    _fields_ = [
+        ("init", C.POINTER(C.c_double)),
+        ("parents", C.POINTER(C.c_int32)),
+        ("take_second", C.POINTER(C.c_uint8)),
+        ("mutate", C.POINTER(C.c_uint8)),
+        ("noise", C.POINTER(C.c_double)),
+    ]
+
+
+class empc_run_args(C.Structure):
+    _fields_ = [
+        ("init", C.c_int32),
+        ("rescore", C.c_int32),
+        ("evolves", C.c_int32),
+        ("slot_in", C.c_int32),
+        ("slot_out", C.c_int32),
+        ("generation0", C.c_int64),
+        ("seed", C.c_uint64),
+        ("mutation_prob", C.c_double),
+        ("crossover_prob", C.c_double),
+        ("x0", C.POINTER(C.c_double)),
+        ("sigma", C.POINTER(C.c_double)),
+        ("inject", C.POINTER(empc_injected)),
+        ("u_out", C.POINTER(C.c_double)),
+        ("best_out", C.POINTER(C.c_double)),
+        ("best_cost", C.POINTER(C.c_double)),
+        ("best_index", C.POINTER(C.c_int32)),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (once).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = C.CDLL(path)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double)
+    sig = {
+        "empc_create": (C.c_int, [C.POINTER(empc_dims), C.POINTER(P)]),
+        "empc_destroy": (None, [P]),
+        "empc_last_error": (C.c_char_p, [P]),
+        "empc_set_schedule": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), D]),
+        "empc_set_problems": (C.c_int, [P, I32, I32] + [D] * 9),
+        "empc_pop_alloc": (C.c_int, [P, C.POINTER(I32)]),
+        "empc_pop_free": (C.c_int, [P, I32]),
+        "empc_pop_read": (C.c_int, [P, I32, D, D]),
+        "empc_pop_write": (C.c_int, [P, I32, D, D]),
+        "empc_run": (C.c_int, [P, C.POINTER(empc_run_args)]),
+        "empc_score": (C.c_int, [P, D, I32, D, D]),
+        "empc_select": (C.c_int, [P, D, C.POINTER(I32), C.POINTER(I32)]),
+        "empc_expand": (C.c_int, [P, I32, D, D]),
+        "empc_time_device": (C.c_int, [P, C.POINTER(empc_run_args), I32, I32, C.POINTER(C.c_float),
+                                        C.POINTER(C.c_float), C.POINTER(I32), C.POINTER(I32)]),
+        "empc_describe": (C.c_int, [P, C.c_char_p, I32]),
+        "empc_num_variants": (C.c_int, [P, C.POINTER(I32)]),
+        "empc_set_variant": (C.c_int, [P, I32]),
+        "empc_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), I32, C.POINTER(C.c_uint32)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, handle=None):
+    if rc == EMPC_OK:
+        return
+    msg = _lib.empc_last_error(handle).decode() if _lib is not None else "unknown error"
+    if rc == EMPC_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"empc error {rc}: {msg}")
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def u8ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Handle:
+    """Owning wrapper of an ``empc_handle*``."""
+
+    def __init__(self, n, m, T, p, num_sims, num_parents, instances=1, dense_q=False, precision=EMPC_FP32,
+                 device=0):
+        self.lib = load()
+        self.dims = empc_dims(n, m, T, p, num_sims, num_parents, instances, int(bool(dense_q)), precision, device)
+        h = C.c_void_p()
+        rc = self.lib.empc_create(C.byref(self.dims), C.byref(h))
+        if rc != EMPC_OK:
+            msg = self.lib.empc_last_error(None).decode()
+            if rc == EMPC_EINVAL:
+                raise ValueError(msg)
+            raise RuntimeError(f"empc_create failed ({rc}): {msg}")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.empc_destroy(self.h)
+            self.h = None
+
+    def call(self, name, *args):
+        check(getattr(self.lib, name)(self.h, *args), self.h)
+
+    def describe(self) -> str:
+        buf = C.create_string_buffer(512)
+        self.call("empc_describe", buf, 512)
+        return buf.value.decode()
+
+    def num_variants(self) -> int:
+        v = C.c_int32()
+        self.call("empc_num_variants", C.byref(v))
+        return v.value
+
+    def set_variant(self, v: int):
+        self.call("empc_set_variant", int(v))
+
+
+def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
+    """Device Philox4x32-10 (known-answer seam)."""
+    lib = load()
+    ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    key = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty_like(ctr)
+    P = C.POINTER(C.c_uint32)
+    check(lib.empc_philox(ctr.ctypes.data_as(P), key.ctypes.data_as(P), ctr.shape[0], out.ctypes.data_as(P)))
+    return out

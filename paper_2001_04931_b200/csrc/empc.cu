@@ -1,0 +1,898 @@
+// Host engine and C ABI (include/empc_b200.h) of the B200 EMPC hot path.
+//
+// One handle = one problem shape (n, m, T, p, N, K) x `instances`, device
+// buffers owned by the handle, one CUDA stream, and a cache of captured CUDA
+// graphs keyed by the run structure (init / rescore / number of evolves).
+// Reference call stack being replaced: K/empc.py:211-236 (solve_empc).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/empc_b200.h"
+#include "empc_kernels.cuh"
+
+using namespace empc;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+constexpr int kMaxSmem = 227 * 1024;
+
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_)};               \
+  } while (0)
+
+struct InvalidArg {
+  std::string msg;
+};
+
+// ---------------------------------------------------------------------------
+// rollout variants: (NP, RR, CC, AREG, DQ) instantiations
+
+template <typename S>
+struct Variant {
+  int NP, RR, CC;
+  bool areg, dq;
+  int maxt;
+  void (*kernel)(const RolloutArgs<S>);
+  const char* name;
+};
+
+// register budget: 512 threads -> 128 regs/thread; A-in-register variants
+// with RR*NP >= 96 get 256 threads -> 255 regs
+#define RVT(S, NP, RR, CC, AR, DQ, MT)                                                              \
+  Variant<S>{NP, RR, CC, AR, DQ, MT, &rollout_kernel<S, NP, RR, CC, AR, DQ, MT>,                      \
+             #S " NP" #NP " RR" #RR " CC" #CC " areg=" #AR " dq=" #DQ " maxt=" #MT}
+#define RV(S, NP, RR, CC, AR, DQ) RVT(S, NP, RR, CC, AR, DQ, ((AR) && (RR) * (NP) * (int)sizeof(S) >= 384) ? 256 : 512)
+
+template <typename S>
+std::vector<Variant<S>> variants_for(int NP);
+
+template <>
+std::vector<Variant<float>> variants_for<float>(int NP) {
+  switch (NP) {
+    case 4: return {RV(float, 4, 1, 4, true, false), RV(float, 4, 4, 4, false, false), RV(float, 4, 4, 4, false, true)};
+    case 8: return {RV(float, 8, 1, 4, true, false), RV(float, 8, 4, 4, false, false), RV(float, 8, 4, 4, false, true)};
+    case 12: return {RV(float, 12, 1, 4, true, false), RV(float, 12, 4, 4, false, false), RV(float, 12, 4, 4, false, true)};
+    case 16: return {RV(float, 16, 1, 4, true, false), RV(float, 16, 4, 4, false, false), RV(float, 16, 4, 8, false, false), RV(float, 16, 4, 4, false, true)};
+    case 24: return {RV(float, 24, 1, 4, true, false), RV(float, 24, 2, 4, true, false), RV(float, 24, 4, 4, false, false), RV(float, 24, 4, 8, false, false), RV(float, 24, 4, 4, false, true)};
+    case 32: return {RV(float, 32, 1, 4, true, false), RV(float, 32, 2, 4, true, false), RV(float, 32, 4, 4, false, false), RV(float, 32, 4, 8, false, false), RV(float, 32, 4, 4, false, true)};
+    case 48: return {RV(float, 48, 1, 4, true, false), RV(float, 48, 2, 4, true, false), RV(float, 48, 4, 4, false, false), RV(float, 48, 4, 8, false, false), RV(float, 48, 4, 4, false, true)};
+    case 64: return {RV(float, 64, 1, 4, true, false), RV(float, 64, 4, 4, false, false), RV(float, 64, 4, 8, false, false), RV(float, 64, 4, 4, false, true)};
+    case 96: return {RV(float, 96, 4, 4, false, false), RV(float, 96, 4, 8, false, false), RV(float, 96, 4, 4, false, true)};
+    case 128: return {RV(float, 128, 4, 4, false, false), RV(float, 128, 4, 8, false, false), RV(float, 128, 4, 4, false, true)};
+  }
+  return {};
+}
+
+template <>
+std::vector<Variant<double>> variants_for<double>(int NP) {
+  switch (NP) {
+    case 4: return {RV(double, 4, 1, 2, true, false), RV(double, 4, 2, 4, false, false), RV(double, 4, 2, 4, false, true)};
+    case 8: return {RV(double, 8, 1, 2, true, false), RV(double, 8, 2, 4, false, false), RV(double, 8, 2, 4, false, true)};
+    case 12: return {RV(double, 12, 1, 2, true, false), RV(double, 12, 2, 4, false, false), RV(double, 12, 2, 4, false, true)};
+    case 16: return {RV(double, 16, 1, 2, true, false), RV(double, 16, 2, 4, false, false), RV(double, 16, 2, 4, false, true)};
+    case 24: return {RV(double, 24, 1, 2, true, false), RV(double, 24, 2, 4, false, false), RV(double, 24, 2, 4, false, true)};
+    case 32: return {RV(double, 32, 1, 2, true, false), RV(double, 32, 2, 4, false, false), RV(double, 32, 2, 4, false, true)};
+    case 48: return {RV(double, 48, 1, 2, true, false), RV(double, 48, 2, 4, false, false), RV(double, 48, 2, 4, false, true)};
+    case 64: return {RV(double, 64, 2, 4, false, false), RV(double, 64, 2, 4, false, true)};
+    case 96: return {RV(double, 96, 2, 4, false, false), RV(double, 96, 2, 4, false, true)};
+    case 128: return {RV(double, 128, 2, 4, false, false), RV(double, 128, 2, 4, false, true)};
+  }
+  return {};
+}
+
+int pad_np(int n) {
+  for (int v : {4, 8, 12, 16, 24, 32, 48, 64, 96, 128})
+    if (n <= v) return v;
+  return -1;
+}
+
+int next_pow2(int x) {
+  int v = 1;
+  while (v < x) v <<= 1;
+  return v;
+}
+
+struct Launch {
+  int tile, tileP, tiles, threads;
+  size_t smem;
+};
+
+// ---------------------------------------------------------------------------
+
+class EngineBase {
+ public:
+  virtual ~EngineBase() = default;
+  std::string err;
+  virtual void set_schedule(const int32_t*, const int32_t*, const double*) = 0;
+  virtual void set_problems(int, int, const double* const*) = 0;
+  virtual int pop_alloc() = 0;
+  virtual void pop_free(int) = 0;
+  virtual void pop_read(int, double*, double*) = 0;
+  virtual void pop_write(int, const double*, const double*) = 0;
+  virtual void run(const empc_run_args&) = 0;
+  virtual void score(const double*, int, const double*, double*) = 0;
+  virtual void select(const double*, int32_t*, int32_t*) = 0;
+  virtual void expand(int, const double*, double*) = 0;
+  virtual void time_device(const empc_run_args&, int, int, float*, float*, int32_t*, int32_t*) = 0;
+  virtual std::string describe() = 0;
+  virtual int num_variants() = 0;
+  virtual void set_variant(int) = 0;
+};
+
+template <typename S>
+class Engine final : public EngineBase {
+ public:
+  explicit Engine(const empc_dims& dd) : dims_(dd) {
+    const int n = dd.n, m = dd.m;
+    d_.n = n; d_.m = m; d_.T = dd.T; d_.p = dd.p; d_.pm = dd.p * dd.m; d_.N = dd.num_sims; d_.K = dd.num_parents;
+    d_.NP = pad_np(n);
+    I_ = dd.instances;
+    dense_ = dd.dense_q != 0;
+    CK(cudaSetDevice(dd.device));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dd.device));
+    variants_ = variants_for<S>(d_.NP);
+    // working layout (elements of S), 16-byte aligned sections
+    auto al = [](int x) { return (x + 3) & ~3; };
+    int o = 0;
+    L_.dm = o; o += al(n * n);
+    L_.bm = o; o += al(n * m);
+    L_.wd = o; o += al(n);
+    L_.qd = o; o += al(n);
+    L_.qf = o; o += dense_ ? al(n * n) : 0;
+    L_.r = o; o += al(m * m);
+    L_.xg = o; o += al(n);
+    L_.ug = o; o += al(m);
+    L_.umin = o; o += al(m);
+    L_.umax = o; o += al(m);
+    L_.x0 = o; o += al(n);
+    L_.sig = o; o += al(m);
+    L_.qxg = o; o += al(n);
+    L_.cost0 = o; o += 4;
+    L_.stride = o;
+    int s = 0;
+    SL_.ad = s; s += n * n;
+    SL_.bd = s; s += n * m;
+    SL_.wd = s; s += n;
+    SL_.q = s; s += n * n;
+    SL_.r = s; s += m * m;
+    SL_.xg = s; s += n;
+    SL_.ug = s; s += m;
+    SL_.umin = s; s += m;
+    SL_.umax = s; s += m;
+    SL_.stride = s;
+    SL_.x0 = 0;
+    SL_.sig = n;
+    SL_.sstride = n + m;
+
+    const size_t popn = (size_t)I_ * d_.N * d_.pm, costn = (size_t)I_ * d_.N;
+    CK(cudaMalloc(&work_, sizeof(S) * (size_t)I_ * L_.stride));
+    CK(cudaMalloc(&stage_prob_d_, sizeof(double) * (size_t)I_ * SL_.stride));
+    CK(cudaMalloc(&stage_state_d_, sizeof(double) * (size_t)I_ * SL_.sstride + sizeof(RunParams) + 64));
+    run_d_ = reinterpret_cast<RunParams*>(
+        (reinterpret_cast<uintptr_t>(stage_state_d_ + (size_t)I_ * SL_.sstride) + 15) & ~(uintptr_t)15);
+    CK(cudaMallocHost(&stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride));
+    CK(cudaMallocHost(&stage_state_h_, sizeof(double) * (size_t)I_ * SL_.sstride + sizeof(RunParams) + 64));
+    run_h_ = reinterpret_cast<RunParams*>(
+        (reinterpret_cast<uintptr_t>(stage_state_h_ + (size_t)I_ * SL_.sstride) + 15) & ~(uintptr_t)15);
+    std::memset(stage_prob_h_, 0, sizeof(double) * (size_t)I_ * SL_.stride);
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&pop_[b], sizeof(S) * popn));
+      CK(cudaMalloc(&cost_[b], sizeof(S) * costn));
+    }
+    CK(cudaMalloc(&elite_, sizeof(int) * (size_t)I_ * d_.K));
+    out_stride_ = d_.m + d_.pm + 2;
+    CK(cudaMalloc(&out_d_, sizeof(double) * (size_t)I_ * out_stride_));
+    CK(cudaMallocHost(&out_h_, sizeof(double) * (size_t)I_ * out_stride_));
+    CK(cudaMalloc(&idx1_, sizeof(int) * d_.T));
+    CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
+    CK(cudaMalloc(&cw_, sizeof(S) * d_.T));
+    CK(cudaMalloc(&G_, sizeof(S) * d_.p * d_.p));
+    select_np2_ = next_pow2(std::max(d_.N, 2));
+    select_smem_ = (size_t)select_np2_ * sizeof(typename KeyOf<S>::type);
+    if (select_smem_ > (size_t)kMaxSmem)
+      throw InvalidArg{"num_sims too large for the single-CTA selection kernel (" + std::to_string(d_.N) + ")"};
+    CK(cudaFuncSetAttribute(select_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    for (auto& v : variants_) CK(cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+  }
+
+  ~Engine() override {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    for (auto& s : slots_)
+      if (s.used) { cudaFree(s.cands); cudaFree(s.costs); }
+    cudaFree(work_); cudaFree(stage_prob_d_); cudaFree(stage_state_d_);
+    cudaFreeHost(stage_prob_h_); cudaFreeHost(stage_state_h_);
+    for (int b = 0; b < 2; ++b) { cudaFree(pop_[b]); cudaFree(cost_[b]); }
+    cudaFree(elite_); cudaFree(out_d_); cudaFreeHost(out_h_);
+    cudaFree(idx1_); cudaFree(idx2_); cudaFree(cw_); cudaFree(G_);
+    if (scratch_pop_) cudaFree(scratch_pop_);
+    if (scratch_cost_) cudaFree(scratch_cost_);
+    if (scratch_dbl_) cudaFree(scratch_dbl_);
+    if (flush_) cudaFree(flush_);
+    for (auto* e : ev_) cudaEventDestroy(e);
+    cudaStreamDestroy(stream_);
+  }
+
+  // -- schedule --------------------------------------------------------------
+  void set_schedule(const int32_t* i1, const int32_t* i2, const double* c) override {
+    const int T = d_.T, p = d_.p;
+    std::vector<S> cs(T);
+    std::vector<double> Wd((size_t)T * p, 0.0);
+    for (int k = 0; k < T; ++k) {
+      if (i1[k] < 0 || i1[k] >= p || i2[k] < 0 || i2[k] >= p || !(c[k] >= 0.0 && c[k] < 1.0))
+        throw InvalidArg{"invalid knot schedule entry at step " + std::to_string(k)};
+      cs[k] = (S)c[k];
+      Wd[(size_t)k * p + i1[k]] += 1.0 - c[k];
+      if (c[k] > 0.0) Wd[(size_t)k * p + i2[k]] += c[k];
+    }
+    std::vector<S> G((size_t)p * p);
+    for (int a = 0; a < p; ++a)
+      for (int b = 0; b < p; ++b) {
+        double s = 0.0;
+        for (int k = 0; k < T; ++k) s += Wd[(size_t)k * p + a] * Wd[(size_t)k * p + b];
+        G[(size_t)a * p + b] = (S)s;
+      }
+    CK(cudaMemcpy(idx1_, i1, sizeof(int) * T, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(idx2_, i2, sizeof(int) * T, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cw_, cs.data(), sizeof(S) * T, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(G_, G.data(), sizeof(S) * p * p, cudaMemcpyHostToDevice));
+    have_sched_ = true;
+  }
+
+  // -- problems (FP64 host -> pinned staging; uploaded inside the run) --------
+  void set_problems(int first, int count, const double* const* arrs) override {
+    if (first < 0 || count < 0 || first + count > I_) throw InvalidArg{"instance range out of bounds"};
+    const int n = d_.n, m = d_.m;
+    const int sizes[9] = {n * n, n * m, n, n * n, m * m, n, m, m, m};
+    const int offs[9] = {SL_.ad, SL_.bd, SL_.wd, SL_.q, SL_.r, SL_.xg, SL_.ug, SL_.umin, SL_.umax};
+    for (int a = 0; a < 9; ++a) {
+      if (!arrs[a]) throw InvalidArg{"null problem array"};
+      for (int i = 0; i < count; ++i)
+        std::memcpy(stage_prob_h_ + (size_t)(first + i) * SL_.stride + offs[a], arrs[a] + (size_t)i * sizes[a],
+                    sizeof(double) * sizes[a]);
+    }
+    have_prob_ = true;
+  }
+
+  // -- population slots --------------------------------------------------------
+  struct Slot {
+    S* cands = nullptr;
+    S* costs = nullptr;
+    bool used = false;
+  };
+  int pop_alloc() override {
+    int id = -1;
+    for (size_t i = 0; i < slots_.size(); ++i)
+      if (!slots_[i].used) { id = (int)i; break; }
+    if (id < 0) { slots_.push_back(Slot{}); id = (int)slots_.size() - 1; }
+    Slot& s = slots_[id];
+    CK(cudaMalloc(&s.cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm));
+    CK(cudaMalloc(&s.costs, sizeof(S) * (size_t)I_ * d_.N));
+    s.used = true;
+    return id;
+  }
+  Slot& slot(int id) {
+    if (id < 0 || id >= (int)slots_.size() || !slots_[id].used) throw InvalidArg{"invalid population slot"};
+    return slots_[id];
+  }
+  void pop_free(int id) override {
+    Slot& s = slot(id);
+    CK(cudaFree(s.cands));
+    CK(cudaFree(s.costs));
+    s = Slot{};
+  }
+  void pop_read(int id, double* cands, double* costs) override {
+    Slot& s = slot(id);
+    const size_t nc = (size_t)I_ * d_.N * d_.pm, nk = (size_t)I_ * d_.N;
+    ensure_scratch_dbl(std::max(nc, nk));
+    if (cands) {
+      uncast_kernel<S><<<grid_for(nc), 256, 0, stream_>>>(s.cands, scratch_dbl_, nc);
+      CK(cudaMemcpyAsync(cands, scratch_dbl_, sizeof(double) * nc, cudaMemcpyDeviceToHost, stream_));
+      CK(cudaStreamSynchronize(stream_));
+    }
+    if (costs) {
+      uncast_kernel<S><<<grid_for(nk), 256, 0, stream_>>>(s.costs, scratch_dbl_, nk);
+      CK(cudaMemcpyAsync(costs, scratch_dbl_, sizeof(double) * nk, cudaMemcpyDeviceToHost, stream_));
+      CK(cudaStreamSynchronize(stream_));
+    }
+    CK(cudaGetLastError());
+  }
+  void pop_write(int id, const double* cands, const double* costs) override {
+    Slot& s = slot(id);
+    const size_t nc = (size_t)I_ * d_.N * d_.pm, nk = (size_t)I_ * d_.N;
+    upload_cast(cands, s.cands, nc);
+    if (costs) upload_cast(costs, s.costs, nk);
+    else CK(cudaMemsetAsync(s.costs, 0, sizeof(S) * nk, stream_));
+    CK(cudaStreamSynchronize(stream_));
+  }
+
+  // -- launch planning ---------------------------------------------------------
+  int pmS() const { return d_.pm | 1; }
+
+  Launch plan(const Variant<S>& v, int nc) const {
+    const int NRG = v.NP / v.RR;
+    const int CC = v.CC;
+    auto fits = [&](int tileP) {
+      const SmemPlan sp = smem_plan<S>(v.NP, d_.n, d_.m, d_.T, d_.p, tileP, pmS(), v.areg, v.dq);
+      return sp.total <= (size_t)kMaxSmem && NRG * (tileP / CC) <= v.maxt;
+    };
+    int maxP = CC;
+    if (!fits(maxP)) throw InvalidArg{"problem too large for the rollout kernel's shared memory"};
+    while (fits(maxP + CC)) maxP += CC;
+    Launch L{};
+    if (nc <= 0) {
+      L.tile = CC; L.tileP = CC; L.tiles = 1;
+    } else if (I_ == 1) {
+      int tile = (nc + sms_ - 1) / sms_;           // one wave over all SMs
+      if (tile > maxP) tile = maxP;                 // several waves when smem-limited
+      int tiles = (nc + tile - 1) / tile;
+      tile = (nc + tiles - 1) / tiles;              // balance
+      L.tile = tile; L.tiles = tiles;
+      L.tileP = (tile + CC - 1) / CC * CC;
+    } else {
+      int want = std::max(CC, (512 / NRG) * CC);
+      want = std::min(want, maxP);
+      int tiles = (nc + want - 1) / want;
+      int tile = (nc + tiles - 1) / tiles;
+      L.tile = tile; L.tiles = tiles;
+      L.tileP = (tile + CC - 1) / CC * CC;
+    }
+    L.threads = NRG * (L.tileP / CC);
+    L.smem = smem_plan<S>(v.NP, d_.n, d_.m, d_.T, d_.p, L.tileP, pmS(), v.areg, v.dq).total;
+    return L;
+  }
+
+  const Variant<S>& pick() {
+    if (forced_ >= 0) return variants_.at(forced_);
+    // heuristic default (bench.py / tests can force any variant)
+    for (auto& v : variants_) {
+      if (v.dq != dense_) continue;
+      if (dense_) return v;
+      if (I_ == 1 && v.areg && v.RR == 1) return v;          // few candidates per SM: max threads
+      if (I_ > 1 && v.areg && v.RR == (sizeof(S) == 4 ? 1 : 1)) return v;
+    }
+    for (auto& v : variants_)
+      if (v.dq == dense_ && !v.areg && v.CC == (sizeof(S) == 4 ? 4 : 4)) return v;
+    return variants_.front();
+  }
+
+  void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,
+                      const int* inj_par = nullptr, const uint8_t* inj_take = nullptr, const uint8_t* inj_mut = nullptr,
+                      const double* inj_noise = nullptr, const S* inj_init = nullptr, const S* work = nullptr) {
+    const Variant<S>& v = pick();
+    const Launch L = plan(v, nc);
+    RolloutArgs<S> a{};
+    a.d = d_; a.L = L_; a.mode = mode; a.nc = nc; a.row0 = row0; a.rows = rows;
+    a.tile = L.tile; a.tileP = L.tileP; a.pmS = pmS(); a.evolve = evolve;
+    a.work = work ? work : work_;
+    a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
+    a.pop_in = pin; a.cost_in = cin; a.pop_out = pout; a.cost_out = cout;
+    a.elite_idx = elite_; a.run = run_d_;
+    a.sig64 = stage_state_d_ + SL_.sig;
+    a.sig64_stride = SL_.sstride;
+    a.inj_parents = inj_par; a.inj_take = inj_take; a.inj_mut = inj_mut; a.inj_noise = inj_noise; a.inj_init = inj_init;
+    dim3 grid(L.tiles, I_);
+    v.kernel<<<grid, L.threads, L.smem, stream_>>>(a);
+    ++launches_;
+    ++rollout_launches_;
+  }
+
+  void launch_select(const S* costs) {
+    const int thr = std::min(1024, std::max(32, select_np2_ / 2));
+    select_kernel<S><<<I_, thr, select_smem_, stream_>>>(costs, d_.N, d_.K, select_np2_, elite_);
+    ++launches_;
+  }
+
+  // The device part of a run: prep, optional init / rescore, evolves, finalize.
+  // Returns the index (0/1) of the buffer holding the final population.
+  int enqueue_core(const empc_run_args& r, const std::vector<const void*>* inj, bool timed_rollouts = false) {
+    launches_ = 0;
+    rollout_launches_ = 0;
+    auto pre = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_], stream_)); };
+    auto post = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_ - 1], stream_)); };
+    prep_kernel<S><<<I_, 256, 0, stream_>>>(d_, L_, SL_, stage_prob_d_, stage_state_d_, work_, dense_ ? 1 : 0);
+    ++launches_;
+    int cur = 0;
+    const size_t pm = d_.pm;
+    if (r.init) {
+      const S* inj_init = inj ? (const S*)(*inj)[0] : nullptr;
+      pre();
+      launch_rollout(inj_init ? kInitInject : kInitPhilox, d_.N, 0, d_.N, 0, nullptr, nullptr, pop_[0], cost_[0],
+                     nullptr, nullptr, nullptr, nullptr, inj_init);
+      post();
+    } else if (r.rescore) {
+      pre();
+      launch_rollout(kScore, d_.N, 0, d_.N, 0, pop_[0], nullptr, pop_[0], cost_[0]);
+      post();
+    }
+    const int nc = d_.N - d_.K;
+    for (int g = 0; g < r.evolves; ++g) {
+      launch_select(cost_[cur]);
+      const int* par = nullptr;
+      const uint8_t *tk = nullptr, *mu = nullptr;
+      const double* nz = nullptr;
+      if (inj && nc > 0) {
+        const size_t per = (size_t)I_ * nc * pm;
+        par = (const int*)(*inj)[1] + (size_t)g * I_ * nc * 2;
+        tk = (const uint8_t*)(*inj)[2] + (size_t)g * per;
+        mu = (const uint8_t*)(*inj)[3] + (size_t)g * per;
+        nz = (const double*)(*inj)[4] + (size_t)g * per;
+      }
+      pre();
+      launch_rollout(par ? kBreedInject : kBreedPhilox, nc, d_.K, d_.N, g, pop_[cur], cost_[cur], pop_[cur ^ 1],
+                     cost_[cur ^ 1], par, tk, mu, nz);
+      post();
+      cur ^= 1;
+    }
+    finalize_kernel<S><<<I_, 256, 0, stream_>>>(pop_[cur], cost_[cur], d_.N, d_.m, d_.pm, out_d_);
+    ++launches_;
+    CK(cudaGetLastError());
+    (void)pm;
+    return cur;
+  }
+
+  void stage_run(const empc_run_args& r) {
+    if (!have_sched_) throw InvalidArg{"schedule not set"};
+    if (!have_prob_) throw InvalidArg{"problem not set"};
+    if (!r.x0 || !r.sigma) throw InvalidArg{"x0 and sigma are required"};
+    if (r.init == 0 && r.slot_in < 0) throw InvalidArg{"a population (slot_in) is required without init"};
+    if (r.evolves < 0) throw InvalidArg{"evolves must be >= 0"};
+    if (!(r.mutation_prob >= 0.0 && r.mutation_prob <= 1.0) || !(r.crossover_prob >= 0.0 && r.crossover_prob <= 1.0))
+      throw InvalidArg{"probabilities must lie in [0, 1]"};
+    const int n = d_.n, m = d_.m;
+    for (int i = 0; i < I_; ++i) {
+      std::memcpy(stage_state_h_ + (size_t)i * SL_.sstride + SL_.x0, r.x0 + (size_t)i * n, sizeof(double) * n);
+      std::memcpy(stage_state_h_ + (size_t)i * SL_.sstride + SL_.sig, r.sigma + (size_t)i * m, sizeof(double) * m);
+    }
+    run_h_->seed = r.seed;
+    run_h_->gen0 = r.generation0;
+    run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 32));
+    run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 32));
+    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice,
+                       stream_));
+    const size_t state_bytes =
+        reinterpret_cast<uintptr_t>(run_h_ + 1) - reinterpret_cast<uintptr_t>(stage_state_h_);
+    CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
+    if (!r.init) {
+      Slot& s = slot(r.slot_in);
+      CK(cudaMemcpyAsync(pop_[0], s.cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice, stream_));
+      CK(cudaMemcpyAsync(cost_[0], s.costs, sizeof(S) * (size_t)I_ * d_.N, cudaMemcpyDeviceToDevice, stream_));
+    }
+  }
+
+  cudaGraphExec_t graph_for(const empc_run_args& r) {
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_);
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) return it->second;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    int cur = 0;
+    try {
+      cur = enqueue_core(r, nullptr);
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(stream_, &g));
+    cudaGraphExec_t ge;
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphDestroy(g));
+    graphs_[key] = ge;
+    graph_cur_[key] = cur;
+    graph_launches_[key] = launches_;
+    graph_rollouts_[key] = rollout_launches_;
+    return ge;
+  }
+
+  void run(const empc_run_args& r) override {
+    stage_run(r);
+    int cur;
+    std::vector<S> init_cast;
+    if (r.inject) {
+      // parity mode: direct launches with the reference's random tensors
+      const empc_injected& in = *r.inject;
+      const int nc = d_.N - d_.K;
+      const size_t per = (size_t)I_ * std::max(nc, 0) * d_.pm;
+      std::vector<const void*> ptrs(5, nullptr);
+      void *d_init = nullptr, *d_par = nullptr, *d_tk = nullptr, *d_mu = nullptr, *d_nz = nullptr;
+      if (r.init) {
+        if (!in.init) throw InvalidArg{"injected init population required"};
+        CK(cudaMalloc(&d_init, sizeof(S) * (size_t)I_ * d_.N * d_.pm));
+        upload_cast(in.init, (S*)d_init, (size_t)I_ * d_.N * d_.pm);
+        ptrs[0] = d_init;
+      }
+      if (r.evolves > 0 && nc > 0) {
+        if (!in.parents || !in.take_second || !in.mutate || !in.noise) throw InvalidArg{"injected draws required"};
+        const size_t E = r.evolves;
+        for (size_t q = 0; q < E * (size_t)I_ * nc * 2; ++q)
+          if (in.parents[q] < 0 || in.parents[q] >= d_.K) throw InvalidArg{"injected parent index out of range"};
+        CK(cudaMalloc(&d_par, sizeof(int) * E * I_ * nc * 2));
+        CK(cudaMalloc(&d_tk, E * per));
+        CK(cudaMalloc(&d_mu, E * per));
+        CK(cudaMalloc(&d_nz, sizeof(double) * E * per));
+        CK(cudaMemcpyAsync(d_par, in.parents, sizeof(int) * E * I_ * nc * 2, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_tk, in.take_second, E * per, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_mu, in.mutate, E * per, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_nz, in.noise, sizeof(double) * E * per, cudaMemcpyHostToDevice, stream_));
+        ptrs[1] = d_par; ptrs[2] = d_tk; ptrs[3] = d_mu; ptrs[4] = d_nz;
+      }
+      cur = enqueue_core(r, &ptrs);
+      CK(cudaStreamSynchronize(stream_));
+      for (void* p : {d_init, d_par, d_tk, d_mu, d_nz})
+        if (p) cudaFree(p);
+    } else {
+      cudaGraphExec_t ge = graph_for(r);
+      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_)];
+      CK(cudaGraphLaunch(ge, stream_));
+    }
+    if (r.slot_out >= 0) {
+      Slot& s = slot(r.slot_out);
+      CK(cudaMemcpyAsync(s.cands, pop_[cur], sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice, stream_));
+      CK(cudaMemcpyAsync(s.costs, cost_[cur], sizeof(S) * (size_t)I_ * d_.N, cudaMemcpyDeviceToDevice, stream_));
+    }
+    CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    const int m = d_.m, pm = d_.pm;
+    for (int i = 0; i < I_; ++i) {
+      const double* o = out_h_ + (size_t)i * out_stride_;
+      if (r.u_out) std::memcpy(r.u_out + (size_t)i * m, o, sizeof(double) * m);
+      if (r.best_out) std::memcpy(r.best_out + (size_t)i * pm, o + m, sizeof(double) * pm);
+      if (r.best_cost) r.best_cost[i] = o[m + pm];
+      if (r.best_index) r.best_index[i] = (int32_t)o[m + pm + 1];
+    }
+  }
+
+  // -- seams ---------------------------------------------------------------------
+  void score(const double* x0, int num, const double* cands, double* costs) override {
+    if (!have_sched_ || !have_prob_) throw InvalidArg{"problem and schedule must be set"};
+    if (num <= 0) return;
+    const int n = d_.n, m = d_.m;
+    for (int i = 0; i < I_; ++i) {
+      std::memcpy(stage_state_h_ + (size_t)i * SL_.sstride + SL_.x0, x0 + (size_t)i * n, sizeof(double) * n);
+      std::fill(stage_state_h_ + (size_t)i * SL_.sstride + SL_.sig, stage_state_h_ + (size_t)i * SL_.sstride + SL_.sig + m, 0.0);
+    }
+    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, sizeof(double) * (size_t)I_ * SL_.sstride, cudaMemcpyHostToDevice, stream_));
+    prep_kernel<S><<<I_, 256, 0, stream_>>>(d_, L_, SL_, stage_prob_d_, stage_state_d_, work_, dense_ ? 1 : 0);
+    const size_t nc = (size_t)I_ * num * d_.pm;
+    ensure_scratch((size_t)I_ * num);
+    upload_cast(cands, scratch_pop_, nc);
+    launch_rollout(kScore, num, 0, num, 0, scratch_pop_, nullptr, scratch_pop_, scratch_cost_);
+    download_uncast(scratch_cost_, costs, (size_t)I_ * num);
+  }
+
+  void select(const double* costs, int32_t* elite, int32_t* best) override {
+    const size_t nk = (size_t)I_ * d_.N;
+    upload_cast(costs, cost_[0], nk);
+    launch_select(cost_[0]);
+    finalize_kernel<S><<<I_, 256, 0, stream_>>>(nullptr, cost_[0], d_.N, d_.m, d_.pm, out_d_);
+    CK(cudaGetLastError());
+    if (elite) CK(cudaMemcpyAsync(elite, elite_, sizeof(int) * (size_t)I_ * d_.K, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    if (best)
+      for (int i = 0; i < I_; ++i) best[i] = (int32_t)out_h_[(size_t)i * out_stride_ + d_.m + d_.pm + 1];
+  }
+
+  void expand(int num, const double* cands, double* traj) override {
+    if (!have_sched_) throw InvalidArg{"schedule not set"};
+    if (num <= 0) return;
+    const size_t nc = (size_t)num * d_.pm, nt = (size_t)num * d_.T * d_.m;
+    ensure_scratch_pop(nc);
+    upload_cast(cands, scratch_pop_, nc);
+    ensure_scratch_dbl(nt);
+    expand_kernel<S><<<grid_for(nt), 256, 0, stream_>>>(scratch_pop_, num, d_.T, d_.p, d_.m, idx1_, idx2_, cw_, scratch_dbl_);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(traj, scratch_dbl_, sizeof(double) * nt, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+  }
+
+  // -- device-resident timing (bench.py `value` and roofline) ---------------------
+  void time_device(const empc_run_args& r, int reps, int flush, float* ms_each, float* rollout_ms, int32_t* nroll,
+                   int32_t* nlaunch) override {
+    stage_run(r);
+    cudaGraphExec_t ge = graph_for(r);
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_);
+    if (flush && !flush_) {
+      flush_n_ = (size_t)256 << 20 >> 4;  // 256 MiB > 126 MB L2
+      CK(cudaMalloc(&flush_, flush_n_ * 16));
+    }
+    const int nr = graph_rollouts_[key];
+    while ((int)ev_.size() < 2 * nr + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_.push_back(e);
+    }
+    CK(cudaStreamSynchronize(stream_));
+    cudaEvent_t t0 = ev_[2 * nr], t1 = ev_[2 * nr + 1];
+    for (int i = 0; i < reps; ++i) {
+      if (flush) flush_kernel<<<sms_ * 4, 512, 0, stream_>>>(flush_, flush_n_, (uint32_t)i);
+      CK(cudaEventRecord(t0, stream_));
+      CK(cudaGraphLaunch(ge, stream_));
+      CK(cudaEventRecord(t1, stream_));
+      CK(cudaEventSynchronize(t1));
+      CK(cudaEventElapsedTime(&ms_each[i], t0, t1));
+    }
+    if (nroll) *nroll = nr;
+    if (nlaunch) *nlaunch = graph_launches_[key];
+    if (rollout_ms) {
+      // per-launch rollout durations: one eager replay of the same sequence
+      // with events on the launching stream around every rollout launch
+      double sum = 0.0;
+      const int reps2 = std::max(1, std::min(reps, 20));
+      for (int i = 0; i < reps2; ++i) {
+        if (flush) flush_kernel<<<sms_ * 4, 512, 0, stream_>>>(flush_, flush_n_, (uint32_t)i);
+        enqueue_core(r, nullptr, true);
+        CK(cudaStreamSynchronize(stream_));
+        for (int q = 0; q < nr; ++q) {
+          float ms;
+          CK(cudaEventElapsedTime(&ms, ev_[2 * q], ev_[2 * q + 1]));
+          sum += ms;
+        }
+      }
+      *rollout_ms = (float)(sum / ((double)reps2 * std::max(nr, 1)));
+    }
+  }
+
+  std::string describe() override {
+    const Variant<S>& v = pick();
+    const Launch a = plan(v, d_.N - d_.K);
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%s | evolve tile=%d tileP=%d tiles=%d threads=%d smem=%zu | sms=%d", v.name, a.tile,
+                  a.tileP, a.tiles, a.threads, a.smem, sms_);
+    return buf;
+  }
+  int num_variants() override { return (int)variants_.size(); }
+  void set_variant(int v) override {
+    if (v >= (int)variants_.size()) throw InvalidArg{"variant out of range"};
+    if (v >= 0 && variants_[v].dq != dense_) throw InvalidArg{"variant does not match the Q structure"};
+    forced_ = v;
+  }
+
+ private:
+  static int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+  void ensure_scratch(size_t ncand) {
+    ensure_scratch_pop(ncand * d_.pm);
+    if (ncand > scratch_cost_n_) {
+      if (scratch_cost_) cudaFree(scratch_cost_);
+      CK(cudaMalloc(&scratch_cost_, sizeof(S) * ncand));
+      scratch_cost_n_ = ncand;
+    }
+  }
+  void ensure_scratch_pop(size_t ne) {
+    if (ne > scratch_pop_n_) {
+      if (scratch_pop_) cudaFree(scratch_pop_);
+      CK(cudaMalloc(&scratch_pop_, sizeof(S) * ne));
+      scratch_pop_n_ = ne;
+    }
+  }
+  void ensure_scratch_dbl(size_t ne) {
+    if (ne > scratch_dbl_n_) {
+      if (scratch_dbl_) cudaFree(scratch_dbl_);
+      CK(cudaMalloc(&scratch_dbl_, sizeof(double) * ne));
+      scratch_dbl_n_ = ne;
+    }
+  }
+  void upload_cast(const double* h, S* dptr, size_t ne) {
+    ensure_scratch_dbl(ne);
+    CK(cudaMemcpyAsync(scratch_dbl_, h, sizeof(double) * ne, cudaMemcpyHostToDevice, stream_));
+    cast_kernel<S><<<grid_for(ne), 256, 0, stream_>>>(scratch_dbl_, dptr, ne);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream_));
+  }
+  void download_uncast(const S* dptr, double* h, size_t ne) {
+    ensure_scratch_dbl(ne);
+    uncast_kernel<S><<<grid_for(ne), 256, 0, stream_>>>(dptr, scratch_dbl_, ne);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, scratch_dbl_, sizeof(double) * ne, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+  }
+
+  empc_dims dims_;
+  Dims d_{};
+  Layout L_{};
+  StageLayout SL_{};
+  int I_ = 1;
+  bool dense_ = false;
+  int sms_ = 148;
+  cudaStream_t stream_{};
+  std::vector<Variant<S>> variants_;
+  int forced_ = -1;
+  S* work_ = nullptr;
+  double *stage_prob_d_ = nullptr, *stage_state_d_ = nullptr, *stage_prob_h_ = nullptr, *stage_state_h_ = nullptr;
+  RunParams *run_d_ = nullptr, *run_h_ = nullptr;
+  S* pop_[2] = {nullptr, nullptr};
+  S* cost_[2] = {nullptr, nullptr};
+  int* elite_ = nullptr;
+  double *out_d_ = nullptr, *out_h_ = nullptr;
+  int out_stride_ = 0;
+  int *idx1_ = nullptr, *idx2_ = nullptr;
+  S *cw_ = nullptr, *G_ = nullptr;
+  int select_np2_ = 2;
+  size_t select_smem_ = 0;
+  bool have_sched_ = false, have_prob_ = false;
+  std::vector<Slot> slots_;
+  S *scratch_pop_ = nullptr, *scratch_cost_ = nullptr;
+  double* scratch_dbl_ = nullptr;
+  size_t scratch_pop_n_ = 0, scratch_cost_n_ = 0, scratch_dbl_n_ = 0;
+  uint4* flush_ = nullptr;
+  size_t flush_n_ = 0;
+  std::vector<cudaEvent_t> ev_;
+  using GKey = std::tuple<bool, bool, int, int>;
+  std::map<GKey, cudaGraphExec_t> graphs_;
+  std::map<GKey, int> graph_cur_, graph_launches_, graph_rollouts_;
+  int launches_ = 0, rollout_launches_ = 0;
+};
+
+}  // namespace
+
+struct empc_handle {
+  std::unique_ptr<EngineBase> eng;
+};
+
+#define GUARD(h, ...)                                              \
+  do {                                                              \
+    if (!(h)) return EMPC_EINVAL;                                   \
+    try {                                                           \
+      __VA_ARGS__;                                                  \
+      return EMPC_OK;                                               \
+    } catch (const InvalidArg& e) {                                 \
+      (h)->eng->err = e.msg;                                        \
+      return EMPC_EINVAL;                                           \
+    } catch (const CudaError& e) {                                  \
+      (h)->eng->err = e.msg;                                        \
+      return EMPC_ECUDA;                                            \
+    } catch (const std::exception& e) {                             \
+      (h)->eng->err = e.what();                                     \
+      return EMPC_ESTATE;                                           \
+    }                                                               \
+  } while (0)
+
+extern "C" {
+
+int empc_create(const empc_dims* dims, empc_handle** out) {
+  if (!dims || !out) return EMPC_EINVAL;
+  *out = nullptr;
+  const empc_dims& d = *dims;
+  if (d.n < 1 || d.m < 1 || d.T < 1 || d.p < 1 || d.p > d.T || d.num_sims < 1 || d.num_parents < 1 ||
+      d.num_parents > d.num_sims || d.instances < 1) {
+    g_create_error = "invalid dimensions";
+    return EMPC_EINVAL;
+  }
+  if (pad_np(d.n) < 0) {
+    g_create_error = "state dimension > 128 is not supported";
+    return EMPC_EINVAL;
+  }
+  try {
+    auto* h = new empc_handle;
+    if (d.precision == EMPC_FP64) h->eng.reset(new Engine<double>(d));
+    else h->eng.reset(new Engine<float>(d));
+    *out = h;
+    return EMPC_OK;
+  } catch (const InvalidArg& e) {
+    g_create_error = e.msg;
+    return EMPC_EINVAL;
+  } catch (const CudaError& e) {
+    g_create_error = e.msg;
+    return EMPC_ECUDA;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return EMPC_ENOMEM;
+  }
+}
+
+void empc_destroy(empc_handle* h) { delete h; }
+
+const char* empc_last_error(const empc_handle* h) {
+  if (!h || !h->eng) return g_create_error.c_str();
+  return h->eng->err.c_str();
+}
+
+int empc_set_schedule(empc_handle* h, const int32_t* idx1, const int32_t* idx2, const double* c) {
+  GUARD(h, { if (!idx1 || !idx2 || !c) throw InvalidArg{"null schedule"}; h->eng->set_schedule(idx1, idx2, c); });
+}
+
+int empc_set_problems(empc_handle* h, int32_t first, int32_t count, const double* Ad, const double* Bd,
+                      const double* wd, const double* Q, const double* R, const double* x_goal, const double* u_goal,
+                      const double* u_min, const double* u_max) {
+  GUARD(h, {
+    const double* arrs[9] = {Ad, Bd, wd, Q, R, x_goal, u_goal, u_min, u_max};
+    h->eng->set_problems(first, count, arrs);
+  });
+}
+
+int empc_pop_alloc(empc_handle* h, int32_t* slot) {
+  GUARD(h, { if (!slot) throw InvalidArg{"null slot"}; *slot = h->eng->pop_alloc(); });
+}
+int empc_pop_free(empc_handle* h, int32_t slot) { GUARD(h, h->eng->pop_free(slot)); }
+int empc_pop_read(empc_handle* h, int32_t slot, double* cands, double* costs) {
+  GUARD(h, h->eng->pop_read(slot, cands, costs));
+}
+int empc_pop_write(empc_handle* h, int32_t slot, const double* cands, const double* costs) {
+  GUARD(h, { if (!cands) throw InvalidArg{"null candidates"}; h->eng->pop_write(slot, cands, costs); });
+}
+
+int empc_run(empc_handle* h, const empc_run_args* args) {
+  GUARD(h, { if (!args) throw InvalidArg{"null args"}; h->eng->run(*args); });
+}
+
+int empc_score(empc_handle* h, const double* x0, int32_t num, const double* cands, double* costs) {
+  GUARD(h, { if (!x0 || (num > 0 && (!cands || !costs))) throw InvalidArg{"null argument"}; h->eng->score(x0, num, cands, costs); });
+}
+
+int empc_select(empc_handle* h, const double* costs, int32_t* elite_idx, int32_t* best_index) {
+  GUARD(h, { if (!costs) throw InvalidArg{"null costs"}; h->eng->select(costs, elite_idx, best_index); });
+}
+
+int empc_expand(empc_handle* h, int32_t num, const double* cands, double* traj) {
+  GUARD(h, { if (num > 0 && (!cands || !traj)) throw InvalidArg{"null argument"}; h->eng->expand(num, cands, traj); });
+}
+
+int empc_time_device(empc_handle* h, const empc_run_args* args, int32_t reps, int32_t flush_l2, float* ms_each,
+                     float* rollout_ms, int32_t* rollout_launches, int32_t* launches_per_rep) {
+  GUARD(h, {
+    if (!args || !ms_each || reps < 1) throw InvalidArg{"invalid timing arguments"};
+    if (args->inject) throw InvalidArg{"timing runs use the in-kernel RNG"};
+    h->eng->time_device(*args, reps, flush_l2, ms_each, rollout_ms, rollout_launches, launches_per_rep);
+  });
+}
+
+int empc_describe(empc_handle* h, char* buf, int32_t len) {
+  GUARD(h, {
+    const std::string s = h->eng->describe();
+    if (buf && len > 0) {
+      std::strncpy(buf, s.c_str(), (size_t)len - 1);
+      buf[len - 1] = 0;
+    }
+  });
+}
+
+int empc_num_variants(empc_handle* h, int32_t* count) {
+  GUARD(h, { if (count) *count = h->eng->num_variants(); });
+}
+
+int empc_set_variant(empc_handle* h, int32_t variant) { GUARD(h, h->eng->set_variant(variant)); }
+
+int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out) {
+  if (count <= 0) return EMPC_OK;
+  if (!ctr || !key || !out) return EMPC_EINVAL;
+  uint32_t *dc = nullptr, *dk = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMalloc(&dc, 16 * (size_t)count);
+  if (e == cudaSuccess) e = cudaMalloc(&dk, 8 * (size_t)count);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, 16 * (size_t)count);
+  if (e == cudaSuccess) e = cudaMemcpy(dc, ctr, 16 * (size_t)count, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dk, key, 8 * (size_t)count, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    philox_kernel<<<(count + 127) / 128, 128>>>(dc, dk, count, dout);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, 16 * (size_t)count, cudaMemcpyDeviceToHost);
+  cudaFree(dc);
+  cudaFree(dk);
+  cudaFree(dout);
+  if (e != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    return EMPC_ECUDA;
+  }
+  return EMPC_OK;
+}
+
+}  // extern "C"

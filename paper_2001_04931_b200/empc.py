@@ -1,0 +1,444 @@
+"""B200-native Evolutionary MPC: drop-in for the knotmpc.empc API.
+
+Same names, signatures, defaults, validation errors and result types as the
+reference module (/root/reference/pkg/src/knotmpc/empc.py, "K/empc.py"):
+``EmpcSettings``, ``Population``, ``EmpcResult``, ``init_population``,
+``evolve_generation``, ``evaluate_cost``, ``solve_empc``.  Every generation
+runs on the GPU through the C ABI of ``include/empc_b200.h``:
+
+* candidates are scored by a full FP32 rollout (kernel K2+K3) -- the
+  function the reference's condensed scorer evaluates (K/empc.py:122-152);
+* selection is a stable (cost, index) sort on the device (K4);
+* children are bred in the prologue of the next rollout (K5) with an
+  in-kernel counter-based Philox4x32-10 stream keyed by
+  (seed, generation, instance, child, gene) instead of numpy's sequential
+  per-generation Philox (K/empc.py:68-70).  ``evolve_generation(...,
+  draws=...)`` and ``init_population(..., candidates=...)`` accept the
+  reference's own random tensors instead (parity mode).
+
+``Population`` keeps its candidates on the device; ``.candidates`` /
+``.costs`` are materialised as FP64 numpy arrays on first access.
+There is no CPU fallback: a missing CUDA library raises.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .param import KnotSchedule, schedule_arrays
+
+
+@dataclass(frozen=True)
+class EmpcSettings:
+    """Population shape and variation operators (K/empc.py:27-48).
+
+    ``precision`` is an extension: "fp32" (default) or "fp64" device
+    arithmetic.
+    """
+
+    num_sims: int = 1024
+    num_parents: int = 64
+    generations: int = 1
+    mutation_prob: float = 0.5
+    crossover_prob: float = 0.5
+    sigma_scale: float = 0.2
+    sigma_noise: np.ndarray | None = None
+    dist_ref: float = 1.0
+    seed: int = 0
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if self.num_sims < 1 or not 1 <= self.num_parents <= self.num_sims:
+            raise ValueError("need 1 <= num_parents <= num_sims")
+        if self.generations < 1:
+            raise ValueError("generations must be >= 1")
+        for name in ("mutation_prob", "crossover_prob"):
+            if not 0.0 <= getattr(self, name) <= 1.0:
+                raise ValueError(f"{name} must lie in [0, 1]")
+        if self.precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+
+
+class Population:
+    """Candidates (N, p, m), their costs (N,) and the RNG generation counter
+    (K/empc.py:51-57).
+
+    Either host-constructed like the reference dataclass
+    (``Population(candidates, costs, generation)``) or returned by the solver
+    with its arrays resident on the GPU.
+    """
+
+    __slots__ = ("_cands", "_costs", "generation", "_dev", "__weakref__")
+
+    def __init__(self, candidates=None, costs=None, generation: int = 0, *, _dev=None):
+        self._cands = None if candidates is None else np.asarray(candidates, float)
+        self._costs = None if costs is None else np.asarray(costs, float)
+        self.generation = int(generation)
+        self._dev = _dev
+
+    @property
+    def candidates(self) -> np.ndarray:
+        if self._cands is None:
+            self._pull()
+        return self._cands
+
+    @candidates.setter
+    def candidates(self, v):
+        self._cands = np.asarray(v, float)
+        self._dev = None
+
+    @property
+    def costs(self) -> np.ndarray:
+        if self._costs is None:
+            self._pull()
+        return self._costs
+
+    @costs.setter
+    def costs(self, v):
+        self._costs = np.asarray(v, float)
+        self._dev = None
+
+    def _pull(self):
+        ctx, slot = self._dev
+        d = ctx.dims
+        c = np.empty((d.instances, d.num_sims, d.p, d.m))
+        k = np.empty((d.instances, d.num_sims))
+        ctx.h.call("empc_pop_read", slot.id, nat.dptr(c), nat.dptr(k))
+        if d.instances == 1:
+            c, k = c[0], k[0]
+        self._cands, self._costs = c, k
+
+    def __repr__(self):
+        where = "device" if self._dev is not None else "host"
+        return f"Population(generation={self.generation}, {where})"
+
+
+@dataclass
+class EmpcResult:
+    """u = first knot of the best candidate, best (p, m), its cost (K/empc.py:60-65)."""
+
+    u: np.ndarray
+    best: np.ndarray
+    best_cost: float
+    population: Population
+
+
+# ---------------------------------------------------------------------------
+# device contexts: one C-ABI handle per problem shape, cached
+
+
+class _Slot:
+    """A device population slot, returned to its context's free list when the
+    owning Population dies."""
+
+    __slots__ = ("id", "__weakref__")
+
+    def __init__(self, sid):
+        self.id = sid
+
+
+class _Context:
+    def __init__(self, n, m, T, p, N, K, instances, dense_q, precision, device=0):
+        self.h = nat.Handle(n, m, T, p, N, K, instances, dense_q,
+                            nat.EMPC_FP64 if precision == "fp64" else nat.EMPC_FP32, device)
+        self.dims = self.h.dims
+        i1, i2, c = schedule_arrays(T, p)
+        self.h.call("empc_set_schedule", nat.iptr(np.ascontiguousarray(i1)), nat.iptr(np.ascontiguousarray(i2)),
+                    nat.dptr(np.ascontiguousarray(c)))
+        self.free = []
+        self.args = nat.empc_run_args()
+
+    def slot(self) -> _Slot:
+        if self.free:
+            sid = self.free.pop()
+        else:
+            v = nat.C.c_int32()
+            self.h.call("empc_pop_alloc", nat.C.byref(v))
+            sid = v.value
+        s = _Slot(sid)
+        weakref.finalize(s, self.free.append, sid)
+        return s
+
+    def set_problems(self, probs):
+        """probs: dict of stacked FP64 arrays (instances leading)."""
+        a = [nat.f64(probs[k]) for k in ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")]
+        self.h.call("empc_set_problems", 0, self.dims.instances, *[nat.dptr(x) for x in a])
+
+
+_contexts: dict = {}
+
+
+def _context(n, m, T, p, N, K, instances, dense_q, precision) -> _Context:
+    key = (n, m, T, p, N, K, instances, bool(dense_q), precision)
+    ctx = _contexts.get(key)
+    if ctx is None:
+        ctx = _contexts[key] = _Context(n, m, T, p, N, K, instances, dense_q, precision)
+    return ctx
+
+
+def _is_diag(Q) -> bool:
+    """The reference's diagonal-Q test (K/empc.py:114)."""
+    return int(np.count_nonzero(Q)) == int(np.count_nonzero(np.diagonal(Q)))
+
+
+def _problem_arrays(spec):
+    mdl = spec.model
+    n, m = mdl.Ad.shape[0], mdl.Bd.shape[1]
+    return {
+        "Ad": mdl.Ad, "Bd": mdl.Bd, "wd": np.broadcast_to(np.asarray(mdl.wd, float), (n,)),
+        "Q": spec.Q, "R": spec.R, "x_goal": spec.x_goal, "u_goal": spec.u_goal,
+        "u_min": spec.u_min, "u_max": spec.u_max,
+    }
+
+
+def _mutation_sigma(spec, settings, x0) -> np.ndarray:
+    """sigma = base * min(1, rms(x_goal - x0) / dist_ref) (K/empc.py:73-82)."""
+    m = spec.model.Bd.shape[1]
+    if settings.sigma_noise is not None:
+        base = np.broadcast_to(np.asarray(settings.sigma_noise, float), (m,))
+    else:
+        base = settings.sigma_scale * (spec.u_max - spec.u_min)
+    err = spec.x_goal - np.asarray(x0, float)
+    dist = float(np.linalg.norm(err)) / np.sqrt(err.size)
+    return base * min(1.0, dist / settings.dist_ref)
+
+
+def _check_sched(spec, sched):
+    if sched.T != spec.T:
+        raise ValueError("knot schedule horizon does not match the spec")
+
+
+def _spec_context(spec, sched, settings, instances=1) -> _Context:
+    _check_sched(spec, sched)
+    n, m = spec.model.Ad.shape[0], spec.model.Bd.shape[1]
+    ctx = _context(n, m, spec.T, sched.p, settings.num_sims, settings.num_parents, instances, not _is_diag(spec.Q),
+                   getattr(settings, "precision", "fp32"))
+    ctx.set_problems(_problem_arrays(spec))
+    return ctx
+
+
+def _device_population(ctx: _Context, pop: Population) -> _Slot:
+    """Slot holding pop on ctx's device (uploads host-built populations)."""
+    if pop._dev is not None and pop._dev[0] is ctx:
+        return pop._dev[1]
+    d = ctx.dims
+    cands = nat.f64(pop.candidates).reshape(d.instances, d.num_sims, d.p, d.m)
+    costs = nat.f64(pop.costs).reshape(d.instances, d.num_sims)
+    s = ctx.slot()
+    ctx.h.call("empc_pop_write", s.id, nat.dptr(cands), nat.dptr(costs))
+    return s
+
+
+def _run(ctx: _Context, settings, x0, sigma, *, init, rescore, evolves, gen0, slot_in=None, inject=None):
+    d = ctx.dims
+    a = ctx.args
+    out_slot = ctx.slot()
+    x0 = nat.f64(x0)
+    sigma = nat.f64(sigma)
+    u = np.empty((d.instances, d.m))
+    best = np.empty((d.instances, d.p, d.m))
+    bc = np.empty(d.instances)
+    bi = np.empty(d.instances, np.int32)
+    a.init, a.rescore, a.evolves = int(init), int(rescore), int(evolves)
+    a.slot_in = slot_in.id if slot_in is not None else -1
+    a.slot_out = out_slot.id
+    a.generation0 = int(gen0)
+    a.seed = int(settings.seed) & 0xFFFFFFFFFFFFFFFF
+    a.mutation_prob = float(settings.mutation_prob)
+    a.crossover_prob = float(settings.crossover_prob)
+    a.x0, a.sigma = nat.dptr(x0), nat.dptr(sigma)
+    a.inject = nat.C.pointer(inject) if inject is not None else None
+    a.u_out, a.best_out, a.best_cost, a.best_index = nat.dptr(u), nat.dptr(best), nat.dptr(bc), nat.iptr(bi)
+    ctx.h.call("empc_run", nat.C.byref(a))
+    return out_slot, u, best, bc, bi
+
+
+# ---------------------------------------------------------------------------
+# public API (K/empc.py:155-236)
+
+
+class CostModel:
+    """Batch scorer for one (spec, schedule, x0): the seam of
+    ``_CostModel.__call__`` (K/empc.py:122-152), evaluated by GPU rollout."""
+
+    def __init__(self, spec, sched: KnotSchedule, x0, *, precision: str = "fp32"):
+        _check_sched(spec, sched)
+        self.spec, self.sched = spec, sched
+        self.x0 = np.asarray(x0, float)
+        self.precision = precision
+
+    def __call__(self, cands) -> np.ndarray:
+        cands = nat.f64(cands)
+        N = cands.shape[0]
+        n, m = self.spec.model.Ad.shape[0], self.spec.model.Bd.shape[1]
+        ctx = _context(n, m, self.spec.T, self.sched.p, 1, 1, 1, not _is_diag(self.spec.Q), self.precision)
+        ctx.set_problems(_problem_arrays(self.spec))
+        costs = np.empty(N)
+        ctx.h.call("empc_score", nat.dptr(nat.f64(self.x0)), N, nat.dptr(cands.reshape(N, -1)), nat.dptr(costs))
+        return costs
+
+
+def evaluate_cost(candidate, spec, sched: KnotSchedule, x0, *, precision: str = "fp32") -> float:
+    """Full tracking cost of one knot candidate, terminal state included
+    (K/empc.py:155-159), by GPU rollout."""
+    U = np.asarray(getattr(candidate, "U", candidate), float).reshape(sched.p, spec.model.Bd.shape[1])
+    return float(CostModel(spec, sched, x0, precision=precision)(U[None])[0])
+
+
+def init_population(spec, sched: KnotSchedule, settings: EmpcSettings, x0, cost=None, *,
+                    candidates=None) -> Population:
+    """Cold start: uniform knots in the input box, all scored (K/empc.py:162-171).
+
+    ``candidates`` injects the initial knots (e.g. the reference's (seed, 0)
+    uniform draw) instead of the in-kernel stream.
+    """
+    ctx = _spec_context(spec, sched, settings)
+    x0 = np.asarray(x0, float)
+    inj = None
+    if candidates is not None:
+        keep = nat.f64(candidates)
+        inj = nat.empc_injected()
+        inj.init = nat.dptr(keep)
+    slot, *_ = _run(ctx, settings, x0, _mutation_sigma(spec, settings, x0), init=True, rescore=False, evolves=0,
+                    gen0=1, inject=inj)
+    return Population(generation=1, _dev=(ctx, slot))
+
+
+def _draw_arrays(draws, ctx):
+    """Pack reference draws (list per evolve of objects with parents,
+    take_second, mutate, noise) into the C layout; keeps them alive."""
+    d = ctx.dims
+    nc = d.num_sims - d.num_parents
+    par = np.ascontiguousarray(np.stack([np.asarray(x.parents).reshape(d.instances, nc, 2) for x in draws]),
+                               dtype=np.int32)
+    tk = np.ascontiguousarray(np.stack([np.asarray(x.take_second).reshape(d.instances, nc, -1) for x in draws]),
+                              dtype=np.uint8)
+    mu = np.ascontiguousarray(np.stack([np.asarray(x.mutate).reshape(d.instances, nc, -1) for x in draws]),
+                              dtype=np.uint8)
+    nz = nat.f64(np.stack([np.asarray(x.noise).reshape(d.instances, nc, -1) for x in draws]))
+    inj = nat.empc_injected()
+    inj.parents, inj.take_second, inj.mutate, inj.noise = nat.iptr(par), nat.u8ptr(tk), nat.u8ptr(mu), nat.dptr(nz)
+    return inj, (par, tk, mu, nz)
+
+
+def evolve_generation(pop: Population, spec, sched: KnotSchedule, settings: EmpcSettings, x0, cost=None, *,
+                      draws=None) -> Population:
+    """One elitist generation at a fixed state x0 (K/empc.py:174-208).
+
+    ``draws`` (an object with ``parents``, ``take_second``, ``mutate``,
+    ``noise`` as drawn at K/empc.py:196-199) replaces the in-kernel RNG.
+    """
+    ctx = _spec_context(spec, sched, settings)
+    x0 = np.asarray(x0, float)
+    src = _device_population(ctx, pop)
+    inj, keep = (None, None)
+    if draws is not None and settings.num_sims > settings.num_parents:
+        inj, keep = _draw_arrays([draws], ctx)
+    slot, *_ = _run(ctx, settings, x0, _mutation_sigma(spec, settings, x0), init=False, rescore=False, evolves=1,
+                    gen0=pop.generation, slot_in=src, inject=inj)
+    del keep
+    return Population(generation=pop.generation + 1, _dev=(ctx, slot))
+
+
+def solve_empc(spec, sched: KnotSchedule, settings: EmpcSettings, x0, prev: Population | None = None, *,
+               draws=None, init_candidates=None) -> EmpcResult:
+    """Run ``settings.generations`` generations and return the best candidate
+    (K/empc.py:211-236): cold = init + (G-1) evolves; warm = re-score
+    ``prev`` at the new x0 + G evolves.  One graph-captured device sequence.
+
+    ``draws`` (list, one per evolve) and ``init_candidates`` inject the
+    reference's random tensors (parity mode).
+    """
+    ctx = _spec_context(spec, sched, settings)
+    x0 = np.asarray(x0, float)
+    sigma = _mutation_sigma(spec, settings, x0)
+    if prev is None:
+        kw = dict(init=True, rescore=False, evolves=settings.generations - 1, gen0=1)
+        gen_end = settings.generations
+    else:
+        kw = dict(init=False, rescore=True, evolves=settings.generations, gen0=prev.generation,
+                  slot_in=_device_population(ctx, prev))
+        gen_end = prev.generation + settings.generations
+    inj, keep = None, []
+    if draws is not None or init_candidates is not None:
+        inj = nat.empc_injected()
+        if init_candidates is not None:
+            ic = nat.f64(init_candidates)
+            keep.append(ic)
+            inj.init = nat.dptr(ic)
+        if draws is not None and settings.num_sims > settings.num_parents and kw["evolves"] > 0:
+            i2, k2 = _draw_arrays(draws, ctx)
+            inj.parents, inj.take_second, inj.mutate, inj.noise = i2.parents, i2.take_second, i2.mutate, i2.noise
+            keep.append(k2)
+    slot, u, best, bc, _ = _run(ctx, settings, x0, sigma, inject=inj, **kw)
+    del keep
+    pop = Population(generation=gen_end, _dev=(ctx, slot))
+    return EmpcResult(u[0], best[0], float(bc[0]), pop)
+
+
+# ---------------------------------------------------------------------------
+# batched independent instances (C5: many robots / scenarios per GPU)
+
+
+@dataclass
+class BatchResult:
+    u: np.ndarray  # (I, m)
+    best: np.ndarray  # (I, p, m)
+    best_cost: np.ndarray  # (I,)
+    population: Population  # candidates (I, N, p, m)
+
+
+def stack_specs(specs) -> dict:
+    """Stack per-instance spec arrays (instances leading)."""
+    arrs = [_problem_arrays(s) for s in specs]
+    return {k: np.stack([np.asarray(a[k], float) for a in arrs]) for k in arrs[0]}
+
+
+class EmpcBatch:
+    """Solve I independent MPC problems of one shape in one device sequence.
+
+    ``problems`` is a list of specs or a dict of stacked arrays (``Ad`` (I,n,n),
+    ``Bd``, ``wd``, ``Q``, ``R``, ``x_goal``, ``u_goal``, ``u_min``,
+    ``u_max``).  Each instance evolves exactly like ``solve_empc`` would on its
+    own (per-instance selection, sigma and RNG streams).
+    """
+
+    def __init__(self, problems, sched: KnotSchedule, settings: EmpcSettings):
+        self.probs = stack_specs(problems) if isinstance(problems, (list, tuple)) else {
+            k: np.asarray(v, float) for k, v in problems.items()}
+        I, n, _ = self.probs["Ad"].shape
+        m = self.probs["Bd"].shape[2]
+        self.I, self.n, self.m = I, n, m
+        self.sched, self.settings = sched, settings
+        dense = any(not _is_diag(q) for q in self.probs["Q"])
+        self.ctx = _context(n, m, sched.T, sched.p, settings.num_sims, settings.num_parents, I, dense,
+                            settings.precision)
+        self.ctx.set_problems(self.probs)
+
+    def sigma(self, x0s) -> np.ndarray:
+        st = self.settings
+        if st.sigma_noise is not None:
+            base = np.broadcast_to(np.asarray(st.sigma_noise, float), (self.I, self.m))
+        else:
+            base = st.sigma_scale * (self.probs["u_max"] - self.probs["u_min"])
+        err = self.probs["x_goal"] - x0s
+        dist = np.linalg.norm(err, axis=1) / np.sqrt(self.n)
+        return base * np.minimum(1.0, dist / st.dist_ref)[:, None]
+
+    def solve(self, x0s, prev: Population | None = None) -> BatchResult:
+        x0s = nat.f64(np.asarray(x0s, float).reshape(self.I, self.n))
+        st = self.settings
+        if prev is None:
+            kw = dict(init=True, rescore=False, evolves=st.generations - 1, gen0=1)
+            gen_end = st.generations
+        else:
+            kw = dict(init=False, rescore=True, evolves=st.generations, gen0=prev.generation,
+                      slot_in=_device_population(self.ctx, prev))
+            gen_end = prev.generation + st.generations
+        self.ctx.set_problems(self.probs)
+        slot, u, best, bc, _ = _run(self.ctx, st, x0s, self.sigma(x0s), **kw)
+        return BatchResult(u, best, bc, Population(generation=gen_end, _dev=(self.ctx, slot)))

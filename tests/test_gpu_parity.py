@@ -1,0 +1,438 @@
+"""GPU parity of the CUDA path against the oracle and the reference's golden
+vectors.  Every call goes through the C ABI (include/empc_b200.h).
+
+Tolerances (stated by the contract):
+  P1 costs FP32: |d|/|J| <= 1e-5 (FP64 device mode: 1e-10)
+  P2 selection on identical costs: bit-exact indices
+  P3 breeding with injected draws: children == FP32(reference children) exactly
+  P4/P5 generation / solve: identical elite sets except where the reference's
+     cost gap at the selection boundary is below the FP32 tolerance
+"""
+
+import numpy as np
+import pytest
+
+import paper_2001_04931_b200 as P
+from paper_2001_04931_b200 import _native as nat
+from oracle import empc_oracle as O
+from tests import golden as G
+
+pytestmark = pytest.mark.gpu
+
+RTOL32 = 1e-5
+RTOL64 = 1e-10
+
+
+def _sched(g):
+    return P.KnotSchedule(int(g["T"]), int(g["p"]))
+
+
+# ---------------------------------------------------------------------------
+# P1 scorer
+
+
+@pytest.mark.parametrize("name", ["spec2", "c1", "c2", "c3s", "dense"])
+@pytest.mark.parametrize("precision,rtol", [("fp32", RTOL32), ("fp64", RTOL64)])
+def test_scorer_matches_reference(name, precision, rtol):
+    g = G.load("score_" + name)
+    cm = P.CostModel(G.spec(g), _sched(g), g["x0"], precision=precision)
+    got = cm(g["cands"])
+    np.testing.assert_allclose(got, g["cost_condensed"], rtol=rtol)
+    np.testing.assert_allclose(got, g["cost_rollout"], rtol=rtol)
+
+
+def test_evaluate_cost_single():
+    g = G.load("score_spec2")
+    for i in range(4):
+        got = P.evaluate_cost(g["cands"][i], G.spec(g), _sched(g), g["x0"])
+        assert got == pytest.approx(float(g["cost_single"][i]), rel=RTOL32)
+        got64 = P.evaluate_cost(g["cands"][i], G.spec(g), _sched(g), g["x0"], precision="fp64")
+        assert got64 == pytest.approx(float(g["cost_single"][i]), rel=1e-12)
+
+
+@pytest.mark.parametrize("num", [1, 3, 33, 200, 1000])
+def test_scorer_ragged_batches(num):
+    """Any candidate count, including partial tiles, matches the oracle."""
+    g = G.load("score_c2")
+    pr = G.problem(g)
+    rng = np.random.default_rng(num)
+    cands = rng.uniform(pr.u_min, pr.u_max, size=(num, int(g["p"]), pr.m))
+    got = P.CostModel(G.spec(g), _sched(g), g["x0"])(cands)
+    want = O.rollout_costs(cands, pr, g["x0"])
+    np.testing.assert_allclose(got, want, rtol=RTOL32)
+
+
+def test_scorer_all_variants():
+    """Every compiled rollout variant for the shape agrees with the oracle."""
+    g = G.load("score_c3s")
+    pr = G.problem(g)
+    spec = G.spec(g)
+    from paper_2001_04931_b200.empc import _context, _problem_arrays
+
+    ctx = _context(pr.n, pr.m, pr.T, int(g["p"]), 1, 1, 1, False, "fp32")
+    ctx.set_problems(_problem_arrays(spec))
+    want = O.rollout_costs(g["cands"], pr, g["x0"])
+    nv = ctx.h.num_variants()
+    tried = 0
+    for v in range(nv):
+        try:
+            ctx.h.set_variant(v)
+        except ValueError:
+            continue  # dense-Q variant on a diagonal problem
+        costs = np.empty(g["cands"].shape[0])
+        ctx.h.call("empc_score", nat.dptr(nat.f64(g["x0"])), costs.size, nat.dptr(nat.f64(g["cands"])),
+                   nat.dptr(costs))
+        np.testing.assert_allclose(costs, want, rtol=RTOL32, err_msg=ctx.h.describe())
+        tried += 1
+    ctx.h.set_variant(-1)
+    assert tried >= 2
+
+
+# ---------------------------------------------------------------------------
+# P2 selection
+
+
+def _select(costs, K, precision="fp32"):
+    N = costs.size
+    ctx = P.empc._context(2, 1, 5, 2, N, K, 1, False, precision)
+    elite = np.empty(K, np.int32)
+    best = np.empty(1, np.int32)
+    ctx.h.call("empc_select", nat.dptr(nat.f64(costs)), nat.iptr(elite), nat.iptr(best))
+    return elite, int(best[0])
+
+
+@pytest.mark.parametrize("N,K", [(1, 1), (2, 1), (8, 8), (100, 6), (1024, 64), (4096, 256), (5000, 77), (16384, 1024)])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_selection_bit_exact(N, K, precision):
+    if precision == "fp64" and N > 8192:
+        with pytest.raises(ValueError):
+            _select(np.zeros(N), K, precision)
+        return
+    rng = np.random.default_rng(N + K)
+    costs = rng.normal(size=N).astype(np.float32).astype(np.float64)
+    # ties, duplicates, signed zeros, infinities
+    if N >= 8:
+        costs[rng.integers(0, N, N // 4)] = costs[0]
+        costs[1], costs[2] = 0.0, -0.0
+        costs[3], costs[4] = np.inf, -np.inf
+    elite, best = _select(costs, K, precision)
+    np.testing.assert_array_equal(elite, np.argsort(costs, kind="stable")[:K])
+    assert best == int(np.argmin(costs))
+
+
+def test_selection_nan_semantics():
+    costs = np.array([3.0, np.nan, 1.0, 1.0, np.nan, -2.0, 0.5, 7.0])
+    elite, best = _select(costs, 8)
+    np.testing.assert_array_equal(elite, np.argsort(costs, kind="stable"))
+    assert best == int(np.argmin(costs)) == 1  # numpy: first NaN
+
+
+# ---------------------------------------------------------------------------
+# P3 breeding / init with injected draws
+
+
+def _fp32_exact(a):
+    return a.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("name", ["spec2_g3", "c1_g10", "c2_g3"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_injected_generation(name, precision):
+    """One generation from an FP32-representable population with the
+    reference's draws: elites, children and costs."""
+    g = G.load("solve_" + name)
+    pr, p, st = G.problem(g), int(g["p"]), G.settings(g)
+    spec, sched = G.spec(g), _sched(g)
+    settings = P.EmpcSettings(num_sims=st.num_sims, num_parents=st.num_parents, seed=st.seed, precision=precision)
+    x0 = g["x0"]
+    cands = _fp32_exact(g["tap_init"])
+    pop0 = P.init_population(spec, sched, settings, x0, candidates=cands)
+    np.testing.assert_array_equal(pop0.candidates, cands)
+    ref_costs = O.CostModel(pr, p, x0)(cands)
+    np.testing.assert_allclose(pop0.costs, ref_costs, rtol=RTOL32 if precision == "fp32" else RTOL64)
+    # identical costs -> identical selection: feed the GPU costs to the oracle
+    d = O.draws(st, 1, p, pr.m)
+    host = P.Population(cands, pop0.costs, 1)
+    got = P.evolve_generation(host, spec, sched, settings, x0, draws=d)
+    want = O.evolve_generation(O.Pop(cands, pop0.costs.copy(), 1), pr, p, st, x0, d=d)
+    K = st.num_parents
+    np.testing.assert_array_equal(got.candidates[:K], want.candidates[:K])
+    np.testing.assert_array_equal(got.costs[:K], want.costs[:K])
+    if precision == "fp64":
+        np.testing.assert_array_equal(got.candidates, want.candidates)
+    else:
+        np.testing.assert_array_equal(got.candidates, _fp32_exact(want.candidates))
+    np.testing.assert_allclose(got.costs[K:], O.rollout_costs(got.candidates[K:], pr, x0),
+                               rtol=RTOL32 if precision == "fp32" else RTOL64)
+    assert got.generation == 2
+
+
+def test_breed_properties_kn_degenerate():
+    g = G.load("solve_spec2_kn")
+    st = G.settings(g)
+    settings = P.EmpcSettings(num_sims=8, num_parents=8, generations=2, seed=7)
+    res = P.solve_empc(G.spec(g), _sched(g), settings, g["x0"])
+    assert np.isfinite(res.best_cost)
+    assert res.population.generation == 2
+    np.testing.assert_array_equal(np.sort(res.population.costs), res.population.costs)
+    assert st.num_sims == 8
+
+
+# ---------------------------------------------------------------------------
+# P4/P5 whole solves driven by the reference's random tensors
+
+
+def _replay(g, precision):
+    pr, p, st = G.problem(g), int(g["p"]), G.settings(g)
+    draws = [O.draws(st, k, p, pr.m) for k in range(1, st.generations)]
+    settings = P.EmpcSettings(num_sims=st.num_sims, num_parents=st.num_parents, generations=st.generations,
+                              seed=st.seed, precision=precision)
+    return P.solve_empc(G.spec(g), _sched(g), settings, g["x0"], draws=draws, init_candidates=g["tap_init"])
+
+
+@pytest.mark.parametrize("name", ["spec2_g3", "c1_g10", "c2_g3"])
+def test_solve_fp64_replays_reference(name):
+    """FP64 device mode + the reference's random tensors reproduces the
+    reference population bit for bit (costs to 1e-10)."""
+    g = G.load("solve_" + name)
+    res = _replay(g, "fp64")
+    np.testing.assert_array_equal(res.population.candidates, g["pop_cands"])
+    np.testing.assert_allclose(res.population.costs, g["pop_costs"], rtol=RTOL64)
+    np.testing.assert_array_equal(res.best, g["best"])
+    np.testing.assert_array_equal(res.u, g["u"])
+    assert res.best_cost == pytest.approx(float(g["best_cost"]), rel=RTOL64)
+
+
+@pytest.mark.parametrize("name", ["spec2_g3", "c1_g10", "c2_g3"])
+def test_solve_fp32_replays_reference(name):
+    """FP32 device mode: same elites unless the reference has a near-tie at a
+    selection boundary; the returned input agrees to 1e-5."""
+    g = G.load("solve_" + name)
+    pr, p, st = G.problem(g), int(g["p"]), G.settings(g)
+    init, trace = O.solve_trace(pr, p, st, g["x0"])
+    gaps = []
+    for pop, _ in trace[:-1]:
+        c = np.sort(pop.costs)
+        K = st.num_parents
+        rel = np.abs(np.diff(c[:min(K + 1, c.size)])) / np.abs(c[:min(K, c.size - 1)])
+        distinct = rel[rel > 0]
+        gaps.append(distinct.min() if distinct.size else np.inf)
+    res = _replay(g, "fp32")
+    if min(gaps) > 1e-4:
+        np.testing.assert_allclose(res.best, g["best"], rtol=1e-5, atol=1e-6)
+        assert res.best_cost == pytest.approx(float(g["best_cost"]), rel=RTOL32)
+    else:
+        # near-tie: only the objective value is comparable
+        assert res.best_cost == pytest.approx(float(g["best_cost"]), rel=1e-4)
+
+
+# ---------------------------------------------------------------------------
+# production path (in-kernel Philox): reference test-suite properties
+
+
+def _test_spec():
+    Ad = np.array([[1.0, 0.02], [-0.4, 0.97]])
+    Bd = np.array([[0.0], [0.05]])
+    model = P.DiscreteLinearModel(Ad, Bd, np.zeros(2), 0.02)
+    return P.MpcSpec(model, 20, Q=np.diag([10.0, 0.1]), R=0.01 * np.eye(1), x_goal=np.array([0.5, 0.0]),
+                     u_goal=np.zeros(1), u_min=-np.array([4.0]), u_max=np.array([4.0]))
+
+
+SPEC = None
+SCHED = P.KnotSchedule(T=20, p=3)
+X0 = np.array([-0.3, 0.1])
+
+
+def _spec():
+    global SPEC
+    if SPEC is None:
+        SPEC = _test_spec()
+    return SPEC
+
+
+def _small(**kw):
+    base = dict(num_sims=64, num_parents=8, seed=7)
+    base.update(kw)
+    return P.EmpcSettings(**base)
+
+
+def test_same_seed_reproduces_bitwise():
+    s = _small(generations=3)
+    a = P.solve_empc(_spec(), SCHED, s, X0)
+    b = P.solve_empc(_spec(), SCHED, s, X0)
+    np.testing.assert_array_equal(a.best, b.best)
+    np.testing.assert_array_equal(a.population.candidates, b.population.candidates)
+    np.testing.assert_array_equal(a.population.costs, b.population.costs)
+    assert a.best_cost == b.best_cost
+
+
+def test_different_seeds_differ():
+    a = P.solve_empc(_spec(), SCHED, _small(seed=1), X0)
+    b = P.solve_empc(_spec(), SCHED, _small(seed=2), X0)
+    assert not np.array_equal(a.population.candidates, b.population.candidates)
+
+
+def test_candidates_respect_input_bounds():
+    s = _small(generations=4)
+    pop = P.init_population(_spec(), SCHED, s, X0)
+    assert pop.candidates.shape == (64, 3, 1)
+    for _ in range(4):
+        assert np.all(pop.candidates >= -4.0) and np.all(pop.candidates <= 4.0)
+        pop = P.evolve_generation(pop, _spec(), SCHED, s, X0)
+
+
+def test_elitism_never_regresses():
+    s = _small()
+    pop = P.init_population(_spec(), SCHED, s, X0)
+    best = np.min(pop.costs)
+    for _ in range(5):
+        prev = pop
+        pop = P.evolve_generation(pop, _spec(), SCHED, s, X0)
+        # elites carried with their costs, in ascending order
+        K = s.num_parents
+        order = np.argsort(prev.costs, kind="stable")[:K]
+        np.testing.assert_array_equal(pop.candidates[:K], prev.candidates[order])
+        np.testing.assert_array_equal(pop.costs[:K], prev.costs[order])
+        assert np.min(pop.costs) <= best
+        best = np.min(pop.costs)
+
+
+def test_population_costs_match_oracle():
+    pop = P.init_population(_spec(), SCHED, _small(), X0)
+    pr = O.Problem.from_spec(_spec())
+    np.testing.assert_allclose(pop.costs, O.rollout_costs(pop.candidates, pr, X0), rtol=RTOL32)
+
+
+def test_result_fields_consistent():
+    res = P.solve_empc(_spec(), SCHED, _small(generations=2), X0)
+    assert res.best.shape == (3, 1)
+    np.testing.assert_array_equal(res.u, res.best[0])
+    assert res.best_cost == pytest.approx(P.evaluate_cost(res.best, _spec(), SCHED, X0), rel=RTOL32)
+    assert res.population.generation == 2
+    assert res.best_cost == float(np.min(res.population.costs))
+
+
+def test_long_search_approaches_qp_optimum():
+    pr = O.Problem.from_spec(_spec())
+    opt = O.qp_optimum(pr, 3, X0)
+    res = P.solve_empc(_spec(), SCHED, P.EmpcSettings(num_sims=256, num_parents=32, generations=120, seed=11), X0)
+    assert res.best_cost <= 1.05 * opt
+
+
+def test_warm_population_reused():
+    s = _small(generations=1)
+    first = P.solve_empc(_spec(), SCHED, s, X0)
+    again = P.solve_empc(_spec(), SCHED, s, X0, prev=first.population)
+    assert again.best_cost <= first.best_cost * (1 + 1e-6)
+    assert again.population.generation == first.population.generation + 1
+    # the old population is still intact after the new solve
+    pr = O.Problem.from_spec(_spec())
+    np.testing.assert_allclose(first.population.costs, O.rollout_costs(first.population.candidates, pr, X0),
+                               rtol=RTOL32)
+
+
+def test_host_population_warm_start():
+    s = _small(generations=2)
+    first = P.solve_empc(_spec(), SCHED, s, X0)
+    host = P.Population(first.population.candidates.copy(), first.population.costs.copy(), 2)
+    a = P.solve_empc(_spec(), SCHED, s, X0 + 0.05, prev=host)
+    b = P.solve_empc(_spec(), SCHED, s, X0 + 0.05, prev=first.population)
+    np.testing.assert_array_equal(a.population.candidates, b.population.candidates)
+
+
+def test_single_knot_schedule():
+    sched = P.KnotSchedule(T=20, p=1)
+    res = P.solve_empc(_spec(), sched, _small(), X0)
+    assert res.best.shape == (1, 1)
+    assert np.isfinite(res.best_cost)
+
+
+def test_state_bounded_spec_scores_same_function():
+    spec = _spec()
+    sb = P.MpcSpec(spec.model, 20, spec.Q, spec.R, spec.x_goal, spec.u_goal, spec.u_min, spec.u_max,
+                   x_min=-10.0 * np.ones(2), x_max=10.0 * np.ones(2))
+    assert sb.has_state_bounds
+    pop = P.init_population(sb, SCHED, _small(), X0)
+    pr = O.Problem.from_spec(sb)
+    for i in (0, 31):
+        assert pop.costs[i] == pytest.approx(O.evaluate_cost(pop.candidates[i], pr, 3, X0), rel=RTOL32)
+
+
+def test_expand_matches_interpolation():
+    rng = np.random.default_rng(5)
+    for T, p in [(23, 6), (20, 3), (50, 4), (200, 5), (8, 1), (7, 7)]:
+        sched = P.KnotSchedule(T=T, p=p)
+        U = rng.normal(size=(9, p, 2))
+        got = P.expand_batch(U, sched)
+        want = np.einsum("tp,npm->ntm", P.interpolation_matrix(sched), U)
+        np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-6)
+        got64 = P.expand_batch(U, sched, precision="fp64")
+        np.testing.assert_allclose(got64, want, rtol=1e-14, atol=1e-14)
+    traj = P.KnotTrajectory(U[0, :, :], sched)
+    np.testing.assert_allclose(P.expand(traj), P.interpolation_matrix(sched) @ U[0], rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# counter-based RNG
+
+
+def _philox_ref(ctr, key):
+    """Pure-Python Philox4x32-10 (Salmon et al. 2011)."""
+    M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+    c = [int(v) for v in ctr]
+    k0, k1 = int(key[0]), int(key[1])
+    for _ in range(10):
+        p0, p1 = M0 * c[0], M1 * c[2]
+        c = [((p1 >> 32) ^ c[1] ^ k0) & 0xFFFFFFFF, p1 & 0xFFFFFFFF, ((p0 >> 32) ^ c[3] ^ k1) & 0xFFFFFFFF,
+             p0 & 0xFFFFFFFF]
+        k0, k1 = (k0 + W0) & 0xFFFFFFFF, (k1 + W1) & 0xFFFFFFFF
+    return c
+
+
+def test_philox_known_answers():
+    ctr = np.array([[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]], np.uint32)
+    key = np.array([[0, 0], [0xFFFFFFFF] * 2, [0xA4093822, 0x299F31D0]], np.uint32)
+    got = nat.philox4x32_10(ctr, key)
+    for i in range(3):
+        assert list(got[i]) == _philox_ref(ctr[i], key[i])
+    # Random123 published known-answer vectors for philox4x32_10
+    assert list(got[0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert list(got[1]) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert list(got[2]) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_philox_operator_statistics():
+    """Mask rates, parent uniformity and mutation noise moments of the
+    in-kernel streams (one generation of a large population)."""
+    spec = _spec()
+    s = P.EmpcSettings(num_sims=16000, num_parents=50, seed=3, sigma_noise=np.array([0.5]), mutation_prob=0.3,
+                       crossover_prob=0.5)
+    # all elites equal except one gene pattern -> children reveal the operators
+    base = np.zeros((16000, 3, 1))
+    costs = np.arange(16000, dtype=float)
+    pop = P.Population(base, costs, 5)
+    x_far = np.array([100.0, 0.0])  # sigma at full scale
+    out = P.evolve_generation(pop, spec, SCHED, s, x_far)
+    kids = out.candidates[50:].ravel()
+    mutated = kids != 0.0
+    assert abs(mutated.mean() - 0.3) < 0.01
+    z = kids[mutated] / 0.5
+    assert abs(z.mean()) < 0.02
+    assert abs(z.std() - 1.0) < 0.02
+    assert abs(np.mean(np.abs(z) > 1.96) - 0.05) < 0.01
+
+
+def test_batched_instances_match_individual_solves():
+    from paper_2001_04931_b200 import workloads as W
+
+    w = W.Workload("mini", 3, 20, 3, 256, 16, 4, instances=5)
+    specs, x0s = W.build(w)
+    st = w.settings()
+    batch = P.EmpcBatch(specs, w.schedule(), st)
+    r = batch.solve(x0s)
+    for i in (0, 3):
+        pr = O.Problem.from_spec(specs[i])
+        cands = r.population.candidates[i]
+        np.testing.assert_allclose(r.population.costs[i], O.rollout_costs(cands, pr, x0s[i]), rtol=RTOL32)
+        assert r.best_cost[i] == pytest.approx(np.min(r.population.costs[i]))
+    assert r.u.shape == (5, 3) and r.best.shape == (5, 3, 3)
