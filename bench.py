@@ -1,0 +1,344 @@
+"""EMPC hot-path benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl ours|reference]
+
+A "step" is one cold ``solve_empc`` (init + G-1 generations + argmin) of the
+configured workload.  Default workload: C3 (24-DoF, T=50, p=4, N=4096,
+K=256, G=10), the north-star per-step latency target.  Under torchrun each
+rank owns one GPU; single-problem workloads run one independent replica per
+rank ("replicas only", weak scaling), the batched C5 workload shards its
+instances across ranks (strong scaling: total instances fixed).
+
+value     = candidate-rollout-steps/s, device-resident (CUDA-event time of the
+            graph-captured solve, inputs already in HBM, L2 flushed between
+            timed solves), summed over ranks / max-over-ranks time.
+e2e       = the same metric through the public Python API (numpy in, numpy
+            out: pinned H2D of the problem + x0, D2H of u / best / cost).
+roofline  = rollout kernel (K2+K3+K5) FP32 FLOP/s vs the measured FFMA peak.
+cpu_baseline / --impl reference = the reference algorithm (CPU oracle port
+            of knotmpc.empc: numpy Philox RNG + condensed quadratic scoring)
+            on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EMPC solve latency per MPC step (ms) and candidate-rollout-steps/sec vs FP32 peak"
+UNIT = "candidate-rollout-steps/s"
+FP32_PEAK_FILE = os.path.join(ROOT, "profiles", "fp32_peak.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "rollout_traffic.json")
+DESCRIPTIONS = {
+    "c1": "2-DoF (4-state) linear joint system, T=20, p=2, N=100, K=6, G=10",
+    "c2": "6-DoF arm, T=50, p=3, N=1024, K=64, G=10",
+    "c3": "24-DoF, T=50, p=4, N=4096, K=256, G=10 (per-step solve latency target < 1 ms)",
+    "c4": "48-DoF, T=200, p=5, N=16384, K=1024, G=10",
+    "c5": "8192 x 12-DoF instances, T=50, p=3, N=512, K=32, G=10",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3", choices=sorted(DESCRIPTIONS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instances", type=int, default=None, help="override the instance count (C5)")
+    ap.add_argument("--variant", type=int, default=-1, help="force a rollout kernel variant")
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def workload(args, rank, world):
+    from paper_2001_04931_b200 import workloads as W
+
+    w = W.WORKLOADS[args.config]
+    if args.instances is not None:
+        w = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=args.instances)
+    if w.instances > 1:  # shard instances across ranks
+        per = (w.instances + world - 1) // world
+        first = rank * per
+        count = max(0, min(per, w.instances - first))
+        specs, x0s = W.build(w, first, count)
+        local = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=count)
+        return w, local, specs, x0s, "strong"
+    specs, x0s = W.build(w)
+    return w, w, specs, x0s, "weak"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 5]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[2:6]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_solve_time(w, specs, x0s, budget_s, max_solves=None):
+    """Time the reference algorithm (oracle port of knotmpc.empc) on the host."""
+    from oracle import empc_oracle as O
+
+    st = O.Settings(num_sims=w.N, num_parents=w.K, generations=w.G, seed=1)
+    pr = O.Problem.from_spec(specs[0])
+    x0 = x0s[0]
+    O.solve_empc(pr, w.p, st, x0)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while not times or (time.perf_counter() - t_start < budget_s and (max_solves is None or len(times) < max_solves)):
+        i = len(times) % len(specs)
+        pr = O.Problem.from_spec(specs[i])
+        t0 = time.perf_counter()
+        O.solve_empc(pr, w.p, st, x0s[i])
+        times.append(time.perf_counter() - t0)
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([d.get("num_threads", 1) for d in threadpool_info() if d.get("internal_api") == "openblas"] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return times, threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2001_04931_b200 import workloads as W
+
+    w, _, specs, x0s, _ = workload(args, 0, 1)
+    per_instance = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, 1)
+    times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=1)
+    budget = 120.0 / max(w.instances, 1) if w.instances > 1 else 120.0
+    steps = max(1, min(args.steps, int(budget / max(times[0], 1e-6))))
+    warm = max(1, min(args.warmup, 3))
+    cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=warm)
+    times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=1e9, max_solves=steps)
+    # one step = one solve of the workload; for batched C5 the instances are
+    # solved one after another (the per-instance time scales linearly)
+    t_step = statistics.mean(times) * w.instances
+    value = per_instance.cand_steps_per_solve * w.instances / t_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(times),
+        "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}", "dof": w.dof, "T": w.T, "p": w.p,
+                   "N": w.N, "K": w.K, "G": w.G, "instances": w.instances},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} cold solves of one instance (oracle port of knotmpc.empc: numpy "
+                                   f"Philox + condensed scoring), scaled x{w.instances} instances"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency_ms": {"median": statistics.median(times) * 1e3},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("CUDA_VISIBLE_DEVICES", str(local))
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    torch.cuda.init()
+
+    import paper_2001_04931_b200 as P
+    from paper_2001_04931_b200 import _native as nat
+    from paper_2001_04931_b200 import empc as E
+
+    w_total, w, specs, x0s, scaling = workload(args, rank, world)
+    sched = w.schedule()
+    st = w.settings()
+    # --- device-resident path: the graph-captured cold solve
+    if w.instances > 1:
+        batch = P.EmpcBatch(specs, sched, st)
+        ctx = batch.ctx
+        sigma = batch.sigma(x0s)
+    else:
+        ctx = E._spec_context(specs[0], sched, st)
+        sigma = E._mutation_sigma(specs[0], st, x0s[0])[None]
+    if args.variant >= 0:
+        ctx.h.set_variant(args.variant)
+    a = nat.empc_run_args()
+    x0c = nat.f64(x0s)
+    sg = nat.f64(sigma)
+    a.init, a.rescore, a.evolves, a.slot_in, a.slot_out = 1, 0, w.G - 1, -1, -1
+    a.generation0, a.seed = 1, st.seed
+    a.mutation_prob, a.crossover_prob = st.mutation_prob, st.crossover_prob
+    a.x0, a.sigma = nat.dptr(x0c), nat.dptr(sg)
+    import ctypes as C
+
+    def time_device(reps, flush=1, want_rollout=False):
+        ms = (C.c_float * reps)()
+        rms = C.c_float(0.0)
+        nr = C.c_int32(0)
+        nl = C.c_int32(0)
+        ctx.h.call("empc_time_device", C.byref(a), reps, flush, ms, C.byref(rms) if want_rollout else None,
+                   C.byref(nr), C.byref(nl))
+        return list(ms), rms.value, nr.value, nl.value
+
+    time_device(max(args.warmup, 3))  # warm-up (graph capture on first use)
+    sampler = ClockSampler(0)
+    t_spin = time.perf_counter()
+    while time.perf_counter() - t_spin < 0.6:  # clocks ramp under load before the timed region
+        time_device(10, flush=0)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ms_each, _, nroll, nlaunch = time_device(args.steps)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    total_ms = sum(ms_each)
+    # roofline pass: per-launch rollout durations (events around each launch)
+    _, rollout_ms, _, _ = time_device(min(args.steps, 20), want_rollout=True)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    units_local = w.cand_steps_per_solve * args.steps
+    units_total = units_local * (world if scaling == "weak" else 1) if w_total.instances == 1 else (
+        w_total.cand_steps_per_solve * args.steps)
+    value = units_total / (total_ms * 1e-3)
+
+    # --- e2e through the public API (numpy in / numpy out)
+    e2e_times = []
+    if w.instances > 1:
+        batch.solve(x0s)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = batch.solve(x0s)
+            e2e_times.append(time.perf_counter() - t0)
+        h2d = batch.probs["Ad"].nbytes + sum(v.nbytes for k, v in batch.probs.items() if k != "Ad") + x0c.nbytes + sg.nbytes
+        d2h = r.u.nbytes + r.best.nbytes + r.best_cost.nbytes + 4 * w.instances
+    else:
+        for _ in range(3):
+            P.solve_empc(specs[0], sched, st, x0s[0])
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = P.solve_empc(specs[0], sched, st, x0s[0])
+            e2e_times.append(time.perf_counter() - t0)
+        pa = E._problem_arrays(specs[0])
+        h2d = sum(np.asarray(v).nbytes for v in pa.values()) + x0s[0].nbytes + sigma.nbytes + 32
+        d2h = r.u.nbytes + r.best.nbytes + 8 + 4
+    e2e_total = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_total], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = units_total / e2e_total
+
+    # --- roofline of the dominant kernel (rollout: K2+K3 with the K5 prologue)
+    flop_per_launch = w.flop_per_candidate * w.scored_per_solve / max(nroll, 1)
+    achieved = flop_per_launch / (rollout_ms * 1e-3) / 1e12
+    peak, peak_src = 72.53, "tools/ffma_peak.cu on a B200 of this pool (no FP32 entry in MEASURED_PEAKS.json)"
+    if os.path.exists(FP32_PEAK_FILE):
+        with open(FP32_PEAK_FILE) as f:
+            pk = json.load(f)
+        peak, peak_src = pk["tflops"], pk.get("source", peak_src)
+    traffic = None
+    if os.path.exists(TRAFFIC_FILE):
+        with open(TRAFFIC_FILE) as f:
+            tr = json.load(f)
+        traffic = tr.get(args.config)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (reference recipe: linearized N-link arms, SURVEY §8d)",
+        "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}", "dof": w.dof, "T": w.T, "p": w.p,
+                   "N": w.N, "K": w.K, "G": w.G, "instances": w_total.instances,
+                   "instances_per_rank": w.instances, "l2": "flushed (256 MiB write) between timed solves",
+                   "kernel_variant": ctx.h.describe()},
+        "latency_ms": {"median": statistics.median(ms_each), "q1": float(np.percentile(ms_each, 25)),
+                       "q3": float(np.percentile(ms_each, 75)), "min": min(ms_each)},
+        "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "rollout_kernel",
+                     "rollout_ms_per_launch": rollout_ms, "rollout_launches_per_step": nroll,
+                     "flop_per_launch": flop_per_launch, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "latency_ms_median": statistics.median(e2e_times) * 1e3, "api": "solve_empc" if w.instances == 1
+                else "EmpcBatch.solve"},
+        "clocks": clocks,
+        "gpu_launches": nlaunch * args.steps,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        from paper_2001_04931_b200 import workloads as W
+
+        one = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, 1)
+        budget = args.cpu_sample_s
+        times, threads = cpu_reference_solve_time(one, specs[:1], x0s[:1], budget_s=budget)
+        cpu_val = one.cand_steps_per_solve / statistics.mean(times)
+        line["cpu_baseline"] = {
+            "value": cpu_val, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} cold solves of one {args.config} instance in {sum(times):.1f}s (oracle port of "
+                      "knotmpc.empc: numpy Philox RNG + condensed-quadratic scoring, OpenBLAS threads)",
+            "ms_per_solve": statistics.mean(times) * 1e3,
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,8 @@ int empc_describe(empc_handle* h, char* buf, int32_t len);
  * (register blocking / A-in-registers choices); -1 restores the heuristic. */
 int empc_num_variants(empc_handle* h, int32_t* count);
 int empc_set_variant(empc_handle* h, int32_t variant);
+/* Rollout CTAs per SM for the launch plan (0 restores the heuristic). */
+int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm);
 
 /* Known-answer seam for the in-kernel counter-based RNG: Philox4x32-10 of
  * `count` (ctr[4], key[2]) pairs evaluated on the device. */

@@ -24,7 +24,7 @@ EXPORTS = (
     "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_problems",
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
-    "empc_set_variant", "empc_philox",
+    "empc_set_variant", "empc_set_occupancy", "empc_philox",
 )
 
 
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "empc_describe": (C.c_int, [P, C.c_char_p, I32]),
         "empc_num_variants": (C.c_int, [P, C.POINTER(I32)]),
         "empc_set_variant": (C.c_int, [P, I32]),
+        "empc_set_occupancy": (C.c_int, [P, I32]),
         "empc_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), I32, C.POINTER(C.c_uint32)]),
     }
     for name, (res, args) in sig.items():
@@ -168,6 +169,9 @@ class Handle:
 
     def set_variant(self, v: int):
         self.call("empc_set_variant", int(v))
+
+    def set_occupancy(self, ctas_per_sm: int):
+        self.call("empc_set_occupancy", int(ctas_per_sm))
 
 
 def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:

@@ -9,15 +9,19 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/empc_b200.h"
+#define EMPC_HOST_TU
 #include "empc_kernels.cuh"
+#include "empc_variants.h"
 
 using namespace empc;
 
@@ -42,73 +46,12 @@ struct InvalidArg {
   std::string msg;
 };
 
-// ---------------------------------------------------------------------------
-// rollout variants: (NP, RR, CC, AREG, DQ) instantiations
-
-template <typename S>
-struct Variant {
-  int NP, RR, CC;
-  bool areg, dq;
-  int maxt;
-  void (*kernel)(const RolloutArgs<S>);
-  const char* name;
-};
-
-// register budget: 512 threads -> 128 regs/thread; A-in-register variants
-// with RR*NP >= 96 get 256 threads -> 255 regs
-#define RVT(S, NP, RR, CC, AR, DQ, MT)                                                              \
-  Variant<S>{NP, RR, CC, AR, DQ, MT, &rollout_kernel<S, NP, RR, CC, AR, DQ, MT>,                      \
-             #S " NP" #NP " RR" #RR " CC" #CC " areg=" #AR " dq=" #DQ " maxt=" #MT}
-#define RV(S, NP, RR, CC, AR, DQ) RVT(S, NP, RR, CC, AR, DQ, ((AR) && (RR) * (NP) * (int)sizeof(S) >= 384) ? 256 : 512)
-
-template <typename S>
-std::vector<Variant<S>> variants_for(int NP);
-
-template <>
-std::vector<Variant<float>> variants_for<float>(int NP) {
-  switch (NP) {
-    case 4: return {RV(float, 4, 1, 4, true, false), RV(float, 4, 4, 4, false, false), RV(float, 4, 4, 4, false, true)};
-    case 8: return {RV(float, 8, 1, 4, true, false), RV(float, 8, 4, 4, false, false), RV(float, 8, 4, 4, false, true)};
-    case 12: return {RV(float, 12, 1, 4, true, false), RV(float, 12, 4, 4, false, false), RV(float, 12, 4, 4, false, true)};
-    case 16: return {RV(float, 16, 1, 4, true, false), RV(float, 16, 4, 4, false, false), RV(float, 16, 4, 8, false, false), RV(float, 16, 4, 4, false, true)};
-    case 24: return {RV(float, 24, 1, 4, true, false), RV(float, 24, 2, 4, true, false), RV(float, 24, 4, 4, false, false), RV(float, 24, 4, 8, false, false), RV(float, 24, 4, 4, false, true)};
-    case 32: return {RV(float, 32, 1, 4, true, false), RV(float, 32, 2, 4, true, false), RV(float, 32, 4, 4, false, false), RV(float, 32, 4, 8, false, false), RV(float, 32, 4, 4, false, true)};
-    case 48: return {RV(float, 48, 1, 4, true, false), RV(float, 48, 2, 4, true, false), RV(float, 48, 4, 4, false, false), RV(float, 48, 4, 8, false, false), RV(float, 48, 4, 4, false, true)};
-    case 64: return {RV(float, 64, 1, 4, true, false), RV(float, 64, 4, 4, false, false), RV(float, 64, 4, 8, false, false), RV(float, 64, 4, 4, false, true)};
-    case 96: return {RV(float, 96, 4, 4, false, false), RV(float, 96, 4, 8, false, false), RV(float, 96, 4, 4, false, true)};
-    case 128: return {RV(float, 128, 4, 4, false, false), RV(float, 128, 4, 8, false, false), RV(float, 128, 4, 4, false, true)};
-  }
-  return {};
-}
-
-template <>
-std::vector<Variant<double>> variants_for<double>(int NP) {
-  switch (NP) {
-    case 4: return {RV(double, 4, 1, 2, true, false), RV(double, 4, 2, 4, false, false), RV(double, 4, 2, 4, false, true)};
-    case 8: return {RV(double, 8, 1, 2, true, false), RV(double, 8, 2, 4, false, false), RV(double, 8, 2, 4, false, true)};
-    case 12: return {RV(double, 12, 1, 2, true, false), RV(double, 12, 2, 4, false, false), RV(double, 12, 2, 4, false, true)};
-    case 16: return {RV(double, 16, 1, 2, true, false), RV(double, 16, 2, 4, false, false), RV(double, 16, 2, 4, false, true)};
-    case 24: return {RV(double, 24, 1, 2, true, false), RV(double, 24, 2, 4, false, false), RV(double, 24, 2, 4, false, true)};
-    case 32: return {RV(double, 32, 1, 2, true, false), RV(double, 32, 2, 4, false, false), RV(double, 32, 2, 4, false, true)};
-    case 48: return {RV(double, 48, 1, 2, true, false), RV(double, 48, 2, 4, false, false), RV(double, 48, 2, 4, false, true)};
-    case 64: return {RV(double, 64, 2, 4, false, false), RV(double, 64, 2, 4, false, true)};
-    case 96: return {RV(double, 96, 2, 4, false, false), RV(double, 96, 2, 4, false, true)};
-    case 128: return {RV(double, 128, 2, 4, false, false), RV(double, 128, 2, 4, false, true)};
-  }
-  return {};
-}
-
 int pad_np(int n) {
   for (int v : {4, 8, 12, 16, 24, 32, 48, 64, 96, 128})
     if (n <= v) return v;
   return -1;
 }
 
-int next_pow2(int x) {
-  int v = 1;
-  while (v < x) v <<= 1;
-  return v;
-}
 
 struct Launch {
   int tile, tileP, tiles, threads;
@@ -135,6 +78,7 @@ class EngineBase {
   virtual std::string describe() = 0;
   virtual int num_variants() = 0;
   virtual void set_variant(int) = 0;
+  virtual void set_occupancy(int) = 0;
 };
 
 template <typename S>
@@ -150,24 +94,13 @@ class Engine final : public EngineBase {
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dd.device));
     variants_ = variants_for<S>(d_.NP);
-    // working layout (elements of S), 16-byte aligned sections
-    auto al = [](int x) { return (x + 3) & ~3; };
-    int o = 0;
-    L_.dm = o; o += al(n * n);
-    L_.bm = o; o += al(n * m);
-    L_.wd = o; o += al(n);
-    L_.qd = o; o += al(n);
-    L_.qf = o; o += dense_ ? al(n * n) : 0;
-    L_.r = o; o += al(m * m);
-    L_.xg = o; o += al(n);
-    L_.ug = o; o += al(m);
-    L_.umin = o; o += al(m);
-    L_.umax = o; o += al(m);
-    L_.x0 = o; o += al(n);
-    L_.sig = o; o += al(m);
-    L_.qxg = o; o += al(n);
-    L_.cost0 = o; o += 4;
-    L_.stride = o;
+    use_pdl_ = std::getenv("EMPC_NO_PDL") == nullptr;
+    phases_ = std::getenv("EMPC_PHASES") != nullptr;
+    incremental_ = std::getenv("EMPC_FULL_SELECT") == nullptr;
+    if (phases_) {
+      dbg_n_ = (size_t)1 << 20;
+      CK(cudaMalloc(&dbg_, dbg_n_ * 8));
+    }
     int s = 0;
     SL_.ad = s; s += n * n;
     SL_.bd = s; s += n * m;
@@ -184,7 +117,6 @@ class Engine final : public EngineBase {
     SL_.sstride = n + m;
 
     const size_t popn = (size_t)I_ * d_.N * d_.pm, costn = (size_t)I_ * d_.N;
-    CK(cudaMalloc(&work_, sizeof(S) * (size_t)I_ * L_.stride));
     CK(cudaMalloc(&stage_prob_d_, sizeof(double) * (size_t)I_ * SL_.stride));
     CK(cudaMalloc(&stage_state_d_, sizeof(double) * (size_t)I_ * SL_.sstride + sizeof(RunParams) + 64));
     run_d_ = reinterpret_cast<RunParams*>(
@@ -199,6 +131,10 @@ class Engine final : public EngineBase {
       CK(cudaMalloc(&cost_[b], sizeof(S) * costn));
     }
     CK(cudaMalloc(&elite_, sizeof(int) * (size_t)I_ * d_.K));
+    qcap_ = std::max(1, d_.N - d_.K);  // every child may qualify: the list never overflows
+    CK(cudaMalloc(&qcount_, sizeof(int) * 2 * (size_t)I_));
+    CK(cudaMemset(qcount_, 0, sizeof(int) * 2 * (size_t)I_));
+    CK(cudaMalloc(&qlist_, sizeof(typename OrdOf<S>::T) * 2 * 2 * (size_t)I_ * qcap_));
     out_stride_ = d_.m + d_.pm + 2;
     CK(cudaMalloc(&out_d_, sizeof(double) * (size_t)I_ * out_stride_));
     CK(cudaMallocHost(&out_h_, sizeof(double) * (size_t)I_ * out_stride_));
@@ -206,11 +142,10 @@ class Engine final : public EngineBase {
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
     CK(cudaMalloc(&cw_, sizeof(S) * d_.T));
     CK(cudaMalloc(&G_, sizeof(S) * d_.p * d_.p));
-    select_np2_ = next_pow2(std::max(d_.N, 2));
-    select_smem_ = (size_t)select_np2_ * sizeof(typename KeyOf<S>::type);
-    if (select_smem_ > (size_t)kMaxSmem)
-      throw InvalidArg{"num_sims too large for the single-CTA selection kernel (" + std::to_string(d_.N) + ")"};
-    CK(cudaFuncSetAttribute(select_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    select_smem_ = select_smem<S>(d_.N);
+    if (select_smem_ > (size_t)kMaxSmem - 1024) throw InvalidArg{"num_sims too large for the selection kernel"};
+    // function attributes are process-wide: always the maximum, never a per-engine size
+    CK(cudaFuncSetAttribute(select_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
     for (auto& v : variants_) CK(cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
   }
 
@@ -218,15 +153,16 @@ class Engine final : public EngineBase {
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     for (auto& s : slots_)
       if (s.used) { cudaFree(s.cands); cudaFree(s.costs); }
-    cudaFree(work_); cudaFree(stage_prob_d_); cudaFree(stage_state_d_);
+    cudaFree(stage_prob_d_); cudaFree(stage_state_d_);
     cudaFreeHost(stage_prob_h_); cudaFreeHost(stage_state_h_);
     for (int b = 0; b < 2; ++b) { cudaFree(pop_[b]); cudaFree(cost_[b]); }
-    cudaFree(elite_); cudaFree(out_d_); cudaFreeHost(out_h_);
+    cudaFree(elite_); cudaFree(qcount_); cudaFree(qlist_); cudaFree(out_d_); cudaFreeHost(out_h_);
     cudaFree(idx1_); cudaFree(idx2_); cudaFree(cw_); cudaFree(G_);
     if (scratch_pop_) cudaFree(scratch_pop_);
     if (scratch_cost_) cudaFree(scratch_cost_);
     if (scratch_dbl_) cudaFree(scratch_dbl_);
     if (flush_) cudaFree(flush_);
+    if (dbg_) cudaFree(dbg_);
     for (auto* e : ev_) cudaEventDestroy(e);
     cudaStreamDestroy(stream_);
   }
@@ -269,6 +205,13 @@ class Engine final : public EngineBase {
         std::memcpy(stage_prob_h_ + (size_t)(first + i) * SL_.stride + offs[a], arrs[a] + (size_t)i * sizes[a],
                     sizeof(double) * sizes[a]);
     }
+    bool rd = true;
+    for (int i = 0; i < I_ && rd; ++i) {
+      const double* R = stage_prob_h_ + (size_t)i * SL_.stride + SL_.r;
+      for (int e = 0; e < m * m; ++e)
+        if (e / m != e % m && R[e] != 0.0) { rd = false; break; }
+    }
+    r_diag_ = rd;
     have_prob_ = true;
   }
 
@@ -325,39 +268,55 @@ class Engine final : public EngineBase {
   }
 
   // -- launch planning ---------------------------------------------------------
-  int pmS() const { return d_.pm | 1; }
+  static int tps_for(int tileP) {
+    constexpr int VEC = Geo<S>::VEC;
+    int t = (tileP + VEC - 1) / VEC * VEC;
+    if ((t / VEC) % 2 == 0) t += VEC;  // odd number of 16-byte chunks: conflict-free rows
+    return t;
+  }
 
   Launch plan(const Variant<S>& v, int nc) const {
     const int NRG = v.NP / v.RR;
     const int CC = v.CC;
+    auto threads_for = [&](int tileP) {
+      const int nl = NRG * (tileP / CC);  // logical threads
+      return v.ks == 1 ? (nl + 31) / 32 * 32 : 2 * ((nl + 15) / 16 * 16);
+    };
     auto fits = [&](int tileP) {
-      const SmemPlan sp = smem_plan<S>(v.NP, d_.n, d_.m, d_.T, d_.p, tileP, pmS(), v.areg, v.dq);
-      return sp.total <= (size_t)kMaxSmem && NRG * (tileP / CC) <= v.maxt;
+      const SmemPlan sp = smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq);
+      return sp.total <= (size_t)kMaxSmem && threads_for(tileP) <= v.maxt;
     };
     int maxP = CC;
-    if (!fits(maxP)) throw InvalidArg{"problem too large for the rollout kernel's shared memory"};
+    if (!fits(maxP)) throw InvalidArg{"problem too large for the rollout kernel (" + std::string(v.name) + ")"};
     while (fits(maxP + CC)) maxP += CC;
     Launch L{};
     if (nc <= 0) {
-      L.tile = CC; L.tileP = CC; L.tiles = 1;
-    } else if (I_ == 1) {
-      int tile = (nc + sms_ - 1) / sms_;           // one wave over all SMs
-      if (tile > maxP) tile = maxP;                 // several waves when smem-limited
+      L.tile = CC; L.tiles = 1;
+    } else if (I_ == 1 || cps_ > 0) {
+      // one wave of `cps` CTAs per SM: small CTAs synchronise only their own
+      // warps each step, so the SM interleaves independent step pipelines
+      const int cps = std::max(1, cps_ > 0 ? cps_ : default_cps(v, nc));
+      int tile = (nc + sms_ * cps - 1) / (sms_ * cps);
+      if (tile > maxP) tile = maxP;        // several waves when smem / threads limit the tile
       int tiles = (nc + tile - 1) / tile;
-      tile = (nc + tiles - 1) / tiles;              // balance
+      tile = (nc + tiles - 1) / tiles;     // balance
       L.tile = tile; L.tiles = tiles;
-      L.tileP = (tile + CC - 1) / CC * CC;
     } else {
       int want = std::max(CC, (512 / NRG) * CC);
       want = std::min(want, maxP);
       int tiles = (nc + want - 1) / want;
-      int tile = (nc + tiles - 1) / tiles;
-      L.tile = tile; L.tiles = tiles;
-      L.tileP = (tile + CC - 1) / CC * CC;
+      L.tile = (nc + tiles - 1) / tiles;
+      L.tiles = tiles;
     }
-    L.threads = NRG * (L.tileP / CC);
-    L.smem = smem_plan<S>(v.NP, d_.n, d_.m, d_.T, d_.p, L.tileP, pmS(), v.areg, v.dq).total;
+    L.tileP = (L.tile + CC - 1) / CC * CC;
+    L.threads = threads_for(L.tileP);
+    L.smem = smem_plan<S>(v.NP, d_.m, d_.T, d_.p, L.tileP, tps_for(L.tileP), v.areg, v.dq).total;
     return L;
+  }
+
+  int default_cps(const Variant<S>& v, int nc) const {
+    (void)v; (void)nc;
+    return 1;
   }
 
   const Variant<S>& pick() {
@@ -366,50 +325,93 @@ class Engine final : public EngineBase {
     for (auto& v : variants_) {
       if (v.dq != dense_) continue;
       if (dense_) return v;
-      if (I_ == 1 && v.areg && v.RR == 1) return v;          // few candidates per SM: max threads
-      if (I_ > 1 && v.areg && v.RR == (sizeof(S) == 4 ? 1 : 1)) return v;
+      if (v.areg && v.RR == 1) return v;  // A in registers, one row per thread: most threads per candidate
     }
     for (auto& v : variants_)
-      if (v.dq == dense_ && !v.areg && v.CC == (sizeof(S) == 4 ? 4 : 4)) return v;
+      if (v.dq == dense_ && !v.areg && v.CC == 4) return v;
     return variants_.front();
   }
 
   void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,
                       const int* inj_par = nullptr, const uint8_t* inj_take = nullptr, const uint8_t* inj_mut = nullptr,
-                      const double* inj_noise = nullptr, const S* inj_init = nullptr, const S* work = nullptr) {
+                      const double* inj_noise = nullptr, const S* inj_init = nullptr) {
     const Variant<S>& v = pick();
     const Launch L = plan(v, nc);
     RolloutArgs<S> a{};
-    a.d = d_; a.L = L_; a.mode = mode; a.nc = nc; a.row0 = row0; a.rows = rows;
-    a.tile = L.tile; a.tileP = L.tileP; a.pmS = pmS(); a.evolve = evolve;
-    a.work = work ? work : work_;
+    a.d = d_; a.SL = SL_; a.mode = mode; a.r_diag = r_diag_ ? 1 : 0;
+    a.nc = nc; a.row0 = row0; a.rows = rows;
+    a.tile = L.tile; a.tileP = L.tileP; a.tPS = tps_for(L.tileP); a.evolve = evolve;
+    a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
     a.pop_in = pin; a.cost_in = cin; a.pop_out = pout; a.cost_out = cout;
     a.elite_idx = elite_; a.run = run_d_;
-    a.sig64 = stage_state_d_ + SL_.sig;
-    a.sig64_stride = SL_.sstride;
     a.inj_parents = inj_par; a.inj_take = inj_take; a.inj_mut = inj_mut; a.inj_noise = inj_noise; a.inj_init = inj_init;
-    dim3 grid(L.tiles, I_);
-    v.kernel<<<grid, L.threads, L.smem, stream_>>>(a);
+    a.dbg = nullptr;
+    a.qcount = (mode == kBreedPhilox || mode == kBreedInject) && incremental_ ? qcount_ + (size_t)(evolve & 1) * I_
+                                                                              : nullptr;
+    a.qlist = (char*)qlist_ + (size_t)(evolve & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
+    a.qcap = qcap_;
+    if (phases_ && (size_t)L.tiles * I_ * 8 <= dbg_n_) {
+      a.dbg = dbg_;
+      dbg_ctas_ = (int)(L.tiles * I_);
+    }
+    launch_ex(v.kernel, dim3(L.tiles, I_), dim3(L.threads), L.smem, pdl_next_, a);
+    pdl_next_ = use_pdl_;
     ++launches_;
     ++rollout_launches_;
   }
 
-  void launch_select(const S* costs) {
-    const int thr = std::min(1024, std::max(32, select_np2_ / 2));
-    select_kernel<S><<<I_, thr, select_smem_, stream_>>>(costs, d_.N, d_.K, select_np2_, elite_);
+  // cudaLaunchKernelEx with programmatic stream serialization: the kernel may
+  // start while its predecessor drains and waits in-kernel (griddepcontrol)
+  template <typename... KArgs, typename... Args>
+  void launch_ex(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, bool pdl, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream_;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+    if (e != cudaSuccess) {
+      char msg[256];
+      std::snprintf(msg, sizeof msg, "cudaLaunchKernelEx(grid=%u,%u block=%u smem=%zu pdl=%d): %s", grid.x, grid.y,
+                    block.x, smem, (int)pdl, cudaGetErrorString(e));
+      throw CudaError{msg};
+    }
+  }
+
+  // evolve index g selects the qualifier-list buffer: rollout g appends to
+  // buffer g & 1, selection g + 1 ranks it and clears buffer (g + 1) & 1
+  void launch_select(const S* costs, int incremental = 0, int g = 0) {
+    const int N = d_.N;
+    const int ctas = I_ == 1 ? std::max(1, std::min(sms_, (N + 15) / 16)) : 1;
+    int* qin = incremental ? qcount_ + (size_t)((g - 1) & 1) * I_ : nullptr;
+    const void* lin = (const char*)qlist_ + (size_t)((g - 1) & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
+    int* qnext = qcount_ + (size_t)(g & 1) * I_;
+    launch_ex(select_kernel<S>, dim3(ctas, I_), dim3(256), select_smem_, pdl_next_, costs, N, d_.K, elite_, incremental,
+              qin, lin, qnext, qcap_);
+    pdl_next_ = use_pdl_;
     ++launches_;
   }
 
   // The device part of a run: prep, optional init / rescore, evolves, finalize.
   // Returns the index (0/1) of the buffer holding the final population.
   int enqueue_core(const empc_run_args& r, const std::vector<const void*>* inj, bool timed_rollouts = false) {
+    struct PdlOff {  // event records between kernels do not mix with programmatic launches
+      bool& flag;
+      bool saved;
+      PdlOff(bool& f, bool off) : flag(f), saved(f) { if (off) flag = false; }
+      ~PdlOff() { flag = saved; }
+    } pdl_guard(use_pdl_, timed_rollouts);
     launches_ = 0;
     rollout_launches_ = 0;
+    pdl_next_ = false;  // the first kernel follows copies, not a kernel
     auto pre = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_], stream_)); };
     auto post = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_ - 1], stream_)); };
-    prep_kernel<S><<<I_, 256, 0, stream_>>>(d_, L_, SL_, stage_prob_d_, stage_state_d_, work_, dense_ ? 1 : 0);
-    ++launches_;
     int cur = 0;
     const size_t pm = d_.pm;
     if (r.init) {
@@ -425,7 +427,8 @@ class Engine final : public EngineBase {
     }
     const int nc = d_.N - d_.K;
     for (int g = 0; g < r.evolves; ++g) {
-      launch_select(cost_[cur]);
+      // after the first evolve of a run, rows [0, K) hold the sorted elites
+      launch_select(cost_[cur], (g > 0 && incremental_) ? 1 : 0, g);
       const int* par = nullptr;
       const uint8_t *tk = nullptr, *mu = nullptr;
       const double* nz = nullptr;
@@ -442,7 +445,9 @@ class Engine final : public EngineBase {
       post();
       cur ^= 1;
     }
-    finalize_kernel<S><<<I_, 256, 0, stream_>>>(pop_[cur], cost_[cur], d_.N, d_.m, d_.pm, out_d_);
+    launch_ex(finalize_kernel<S>, dim3(I_), dim3(256), 0, pdl_next_, (const S*)pop_[cur], (const S*)cost_[cur], d_.N,
+              d_.m, d_.pm, out_d_);
+    pdl_next_ = false;
     ++launches_;
     CK(cudaGetLastError());
     (void)pm;
@@ -479,7 +484,7 @@ class Engine final : public EngineBase {
   }
 
   cudaGraphExec_t graph_for(const empc_run_args& r) {
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_);
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;
     cudaGraph_t g;
@@ -540,7 +545,7 @@ class Engine final : public EngineBase {
         if (p) cudaFree(p);
     } else {
       cudaGraphExec_t ge = graph_for(r);
-      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_)];
+      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_)];
       CK(cudaGraphLaunch(ge, stream_));
     }
     if (r.slot_out >= 0) {
@@ -571,18 +576,21 @@ class Engine final : public EngineBase {
     }
     CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice, stream_));
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, sizeof(double) * (size_t)I_ * SL_.sstride, cudaMemcpyHostToDevice, stream_));
-    prep_kernel<S><<<I_, 256, 0, stream_>>>(d_, L_, SL_, stage_prob_d_, stage_state_d_, work_, dense_ ? 1 : 0);
     const size_t nc = (size_t)I_ * num * d_.pm;
     ensure_scratch((size_t)I_ * num);
     upload_cast(cands, scratch_pop_, nc);
+    pdl_next_ = false;
     launch_rollout(kScore, num, 0, num, 0, scratch_pop_, nullptr, scratch_pop_, scratch_cost_);
+    pdl_next_ = false;
     download_uncast(scratch_cost_, costs, (size_t)I_ * num);
   }
 
   void select(const double* costs, int32_t* elite, int32_t* best) override {
     const size_t nk = (size_t)I_ * d_.N;
     upload_cast(costs, cost_[0], nk);
-    launch_select(cost_[0]);
+    pdl_next_ = false;
+    launch_select(cost_[0], 0);
+    pdl_next_ = false;
     finalize_kernel<S><<<I_, 256, 0, stream_>>>(nullptr, cost_[0], d_.N, d_.m, d_.pm, out_d_);
     CK(cudaGetLastError());
     if (elite) CK(cudaMemcpyAsync(elite, elite_, sizeof(int) * (size_t)I_ * d_.K, cudaMemcpyDeviceToHost, stream_));
@@ -610,7 +618,7 @@ class Engine final : public EngineBase {
                    int32_t* nlaunch) override {
     stage_run(r);
     cudaGraphExec_t ge = graph_for(r);
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_);
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_);
     if (flush && !flush_) {
       flush_n_ = (size_t)256 << 20 >> 4;  // 256 MiB > 126 MB L2
       CK(cudaMalloc(&flush_, flush_n_ * 16));
@@ -650,6 +658,25 @@ class Engine final : public EngineBase {
       }
       *rollout_ms = (float)(sum / ((double)reps2 * std::max(nr, 1)));
     }
+    if (phases_ && dbg_ctas_ > 0) {
+      // phase durations of the last rollout launch: mean and max over CTAs, relative to the earliest start
+      std::vector<unsigned long long> t((size_t)dbg_ctas_ * 8);
+      CK(cudaMemcpy(t.data(), dbg_, t.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < dbg_ctas_; ++c) t0 = std::min(t0, t[(size_t)c * 8]);
+      double mean[7] = {0}, mx[7] = {0};
+      for (int c = 0; c < dbg_ctas_; ++c)
+        for (int i = 0; i < 7; ++i) {
+          const double v = (double)(t[(size_t)c * 8 + i] - t0) * 1e-3;
+          mean[i] += v / dbg_ctas_;
+          mx[i] = std::max(mx[i], v);
+        }
+      std::fprintf(stderr, "phases(us from first CTA start) start/p0/wait/genes/bu/loop/end mean:");
+      for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %.2f", mean[i]);
+      std::fprintf(stderr, " | max:");
+      for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %.2f", mx[i]);
+      std::fprintf(stderr, "\n");
+    }
   }
 
   std::string describe() override {
@@ -661,6 +688,10 @@ class Engine final : public EngineBase {
     return buf;
   }
   int num_variants() override { return (int)variants_.size(); }
+  void set_occupancy(int cps) override {
+    if (cps < 0 || cps > 32) throw InvalidArg{"ctas_per_sm must lie in [0, 32]"};
+    cps_ = cps;
+  }
   void set_variant(int v) override {
     if (v >= (int)variants_.size()) throw InvalidArg{"variant out of range"};
     if (v >= 0 && variants_[v].dq != dense_) throw InvalidArg{"variant does not match the Q structure"};
@@ -708,7 +739,6 @@ class Engine final : public EngineBase {
 
   empc_dims dims_;
   Dims d_{};
-  Layout L_{};
   StageLayout SL_{};
   int I_ = 1;
   bool dense_ = false;
@@ -716,19 +746,25 @@ class Engine final : public EngineBase {
   cudaStream_t stream_{};
   std::vector<Variant<S>> variants_;
   int forced_ = -1;
-  S* work_ = nullptr;
+  int cps_ = 0;  // CTAs per SM for the rollout (0: heuristic)
+  bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
+  unsigned long long* dbg_ = nullptr;
+  size_t dbg_n_ = 0;
+  int dbg_ctas_ = 0;
   double *stage_prob_d_ = nullptr, *stage_state_d_ = nullptr, *stage_prob_h_ = nullptr, *stage_state_h_ = nullptr;
   RunParams *run_d_ = nullptr, *run_h_ = nullptr;
   S* pop_[2] = {nullptr, nullptr};
   S* cost_[2] = {nullptr, nullptr};
   int* elite_ = nullptr;
+  int* qcount_ = nullptr;
+  void* qlist_ = nullptr;
+  int qcap_ = 0;
   double *out_d_ = nullptr, *out_h_ = nullptr;
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr;
   S *cw_ = nullptr, *G_ = nullptr;
-  int select_np2_ = 2;
   size_t select_smem_ = 0;
-  bool have_sched_ = false, have_prob_ = false;
+  bool have_sched_ = false, have_prob_ = false, r_diag_ = true;
   std::vector<Slot> slots_;
   S *scratch_pop_ = nullptr, *scratch_cost_ = nullptr;
   double* scratch_dbl_ = nullptr;
@@ -736,7 +772,7 @@ class Engine final : public EngineBase {
   uint4* flush_ = nullptr;
   size_t flush_n_ = 0;
   std::vector<cudaEvent_t> ev_;
-  using GKey = std::tuple<bool, bool, int, int>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int>;
   std::map<GKey, cudaGraphExec_t> graphs_;
   std::map<GKey, int> graph_cur_, graph_launches_, graph_rollouts_;
   int launches_ = 0, rollout_launches_ = 0;
@@ -870,6 +906,8 @@ int empc_num_variants(empc_handle* h, int32_t* count) {
 }
 
 int empc_set_variant(empc_handle* h, int32_t variant) { GUARD(h, h->eng->set_variant(variant)); }
+
+int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm) { GUARD(h, h->eng->set_occupancy(ctas_per_sm)); }
 
 int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out) {
   if (count <= 0) return EMPC_OK;

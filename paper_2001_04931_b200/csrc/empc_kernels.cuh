@@ -1,25 +1,23 @@
 // Kernels of the B200 EMPC hot path.  Reference: /root/reference/pkg/src/
 // knotmpc/empc.py (K/empc.py) and param.py (K/param.py).
 //
-//   prep_kernel     per-solve problem/state conversion (FP64 host layout ->
-//                   working layout, Delta = Ad - I, cost of x0)
-//   rollout_kernel  K2+K3 (+K5 prologue): breed/init/load candidates, B at
-//                   the knots, horizon recursion, fused quadratic cost
-//   select_kernel   K4: stable top-K (argsort(kind="stable")[:K])
+//   rollout_kernel  K2+K3 (+K5 prologue): breed / init / load candidates,
+//                   B at the knots, horizon recursion, fused quadratic cost.
+//                   Reads the FP64 problem staging directly (no prep pass).
+//   select_kernel   K4: stable top-K (argsort(kind="stable")[:K]) by a
+//                   bitwise radix search for the K-th smallest (cost, index)
+//                   key, compaction, and rank-by-counting of the K survivors
 //   finalize_kernel argmin + best candidate extraction (K/empc.py:234-236)
 //   expand_kernel   K1: knots -> per-step inputs (K/param.py:114-116)
 #pragma once
+
+#include <type_traits>
 
 #include "empc_device.cuh"
 
 namespace empc {
 
 enum Mode : int { kScore = 0, kInitPhilox = 1, kInitInject = 2, kBreedPhilox = 3, kBreedInject = 4 };
-
-// Offsets (elements of S) of one instance's working block.
-struct Layout {
-  int dm, bm, wd, qd, qf, r, xg, ug, umin, umax, x0, sig, qxg, cost0, stride;
-};
 
 // Offsets (doubles) of the FP64 staging block of one instance (C-ABI order).
 struct StageLayout {
@@ -40,80 +38,21 @@ struct Dims {
   int n, m, T, p, pm, N, K, NP;
 };
 
-// ---------------------------------------------------------------------------
-// prep: one CTA per instance.
-
-template <typename S>
-__global__ void prep_kernel(Dims d, Layout L, StageLayout SL, const double* __restrict__ stage_prob,
-                            const double* __restrict__ stage_state, S* __restrict__ work, int dense_q) {
-  const int inst = blockIdx.x;
-  const double* P = stage_prob + (size_t)inst * SL.stride;
-  const double* X = stage_state + (size_t)inst * SL.sstride;
-  S* w = work + (size_t)inst * L.stride;
-  const int n = d.n, m = d.m;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    w[L.dm + e] = (S)(P[SL.ad + e] - (i == j ? 1.0 : 0.0));  // Delta = Ad - I (FP64 subtraction)
-    if (dense_q) w[L.qf + e] = (S)P[SL.q + e];
-  }
-  for (int e = threadIdx.x; e < n * m; e += blockDim.x) w[L.bm + e] = (S)P[SL.bd + e];
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) w[L.r + e] = (S)P[SL.r + e];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    w[L.wd + i] = (S)P[SL.wd + i];
-    w[L.qd + i] = (S)P[SL.q + i * n + i];
-    w[L.xg + i] = (S)P[SL.xg + i];
-    w[L.x0 + i] = (S)X[SL.x0 + i];
-    if (dense_q) {
-      double s = 0.0;
-      for (int j = 0; j < n; ++j) s += P[SL.q + i * n + j] * P[SL.xg + j];
-      w[L.qxg + i] = (S)s;
-    }
-  }
-  for (int l = threadIdx.x; l < m; l += blockDim.x) {
-    w[L.ug + l] = (S)P[SL.ug + l];
-    w[L.umin + l] = (S)P[SL.umin + l];
-    w[L.umax + l] = (S)P[SL.umax + l];
-    w[L.sig + l] = (S)X[SL.sig + l];
-  }
-  // cost of x_0 (the k = 0 state term of K/empc.py:113-118), FP64, fixed-order
-  // reduction so the result is deterministic
-  __shared__ double red[256];
-  double part = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double ei = X[SL.x0 + i] - P[SL.xg + i];
-    if (dense_q) {
-      double qe = 0.0;
-      for (int j = 0; j < n; ++j) qe += P[SL.q + i * n + j] * (X[SL.x0 + j] - P[SL.xg + j]);
-      part += ei * qe;
-    } else {
-      part += P[SL.q + i * n + i] * ei * ei;
-    }
-  }
-  red[threadIdx.x] = part;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) w[L.cost0] = (S)red[0];
-}
-
-// ---------------------------------------------------------------------------
-// rollout: K2 + K3 with the K5 breed / init prologue.
-
 template <typename S>
 struct RolloutArgs {
   Dims d;
-  Layout L;
+  StageLayout SL;
   int mode;
-  int nc;     // candidates scored per instance by this launch
-  int row0;   // first scored row in the population arrays (K when breeding)
-  int rows;   // rows per instance of the population arrays
-  int tile;   // candidates per CTA
-  int tileP;  // tile rounded up to CC
-  int pmS;    // padded gene stride of the smem knot buffer (odd)
-  int evolve; // index of this evolve within the run (RNG generation = gen0 + evolve)
-  const S* work;
+  int r_diag;  // R diagonal: input cost fast path
+  int nc;      // candidates scored per instance by this launch
+  int row0;    // first scored row in the population arrays (K when breeding)
+  int rows;    // rows per instance of the population arrays
+  int tile;    // candidates per CTA
+  int tileP;   // tile rounded up to CC
+  int tPS;     // padded candidate stride of the knot / drive buffers
+  int evolve;  // index of this evolve within the run (RNG generation = gen0 + evolve)
+  const double* prob;   // FP64 problem staging, instances x SL.stride
+  const double* state;  // FP64 state staging (x0, sigma), instances x SL.sstride
   const int* idx1;
   const int* idx2;
   const S* cw;
@@ -129,72 +68,186 @@ struct RolloutArgs {
   const uint8_t* inj_mut;
   const double* inj_noise;
   const S* inj_init;
-  const double* sig64;  // FP64 sigma (staging) for reference-exact injected mutation
-  int sig64_stride;
+  unsigned long long* dbg;  // optional per-CTA phase timestamps (globaltimer, ns)
+  int* qcount;              // per instance: children that beat the K-th elite (incremental selection)
+  void* qlist;              // per instance: [qcap] (ord key, row) pairs
+  int qcap;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define EMPC_MARK(I)                                                                                  \
+  if (a.dbg != nullptr && threadIdx.x == 0)                                                          \
+    a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (I)] = gtimer();
+
+template <typename S>
+struct Geo {
+  static constexpr int VEC = 16 / (int)sizeof(S);  // elements per 16-byte LDS
+  // padded state stride: odd number of 16-byte chunks -> conflict-free rows
+  __host__ __device__ static constexpr int nps(int NP) { return ((NP / VEC) % 2 == 0) ? NP + VEC : NP; }
 };
 
 // Shared memory plan (host and device agree on it).
 struct SmemPlan {
-  size_t us, but, xt, dt, qt, sched, g, cu, src, total;
+  size_t us, but, xc, as, qs, sched, g, cu, src, cv, total;
 };
 
 template <typename S>
-__host__ __device__ inline SmemPlan smem_plan(int NP, int n, int m, int T, int p, int tileP, int pmS, bool areg,
-                                              bool dq) {
+__host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int tileP, int tPS, bool areg, bool dq) {
   auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const int NPS = Geo<S>::nps(NP);
+  (void)areg;
   SmemPlan s;
-  s.us = al((size_t)tileP * pmS * sizeof(S));
-  s.but = al((size_t)p * NP * tileP * sizeof(S));
-  const size_t xt_elems = (size_t)2 * NP * tileP;
-  const size_t ru_elems = (size_t)tileP * m;
-  s.xt = al((xt_elems > ru_elems ? xt_elems : ru_elems) * sizeof(S));
-  s.dt = areg ? 0 : al((size_t)NP * NP * sizeof(S));
-  s.qt = dq ? al((size_t)NP * NP * sizeof(S)) : 0;
+  s.us = al((size_t)p * m * tPS * sizeof(S));
+  s.but = al((size_t)p * NP * tPS * sizeof(S));
+  const size_t xc = (size_t)2 * tileP * NPS, bs = (size_t)NP * (m + 1);
+  s.xc = al((xc > bs ? xc : bs) * sizeof(S));
+  s.as = al((size_t)NP * NPS * sizeof(S));  // A staging (copied to registers by AREG variants)
+  s.qs = dq ? al((size_t)NP * NPS * sizeof(S)) : 0;
   s.sched = al((size_t)T * (2 * sizeof(int) + sizeof(S)));
-  s.g = al((size_t)p * p * sizeof(S));
+  s.g = al((size_t)(p * p + 2) * sizeof(S));
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
-  s.total = s.us + s.but + s.xt + s.dt + s.qt + s.sched + s.g + s.cu + s.src;
-  (void)n;
+  s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S));
+  s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv;
   return s;
 }
 
-template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int MAXT>
-__global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
+__device__ __forceinline__ uint32_t ord_key(float c) { return ord32(c); }
+__device__ __forceinline__ uint64_t ord_key(double c) { return ord64(c); }
+
+// Programmatic dependent launch: wait for the producer grid (no-op when the
+// kernel was launched without the attribute) / let the consumer grid start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// rollout: K2 + K3 with the K5 breed / init prologue.
+//
+// Thread (rg, cg) owns rows {rg + r*NRG} (r < RR) of candidates
+// [cg*CC, cg*CC + CC) of the tile.  States live in registers (xo) and, for
+// the all-to-all of the matvec, in a double-buffered candidate-major smem
+// tile XC[buf][cand][NPS]; every x load is a 16-byte broadcast with a
+// compile-time offset.  A (as Delta = Ad - I) is in registers (AREG) or in
+// smem rows As[row][NPS].  With KS = 2 the column range of the matvec is
+// split over the lane pair (l, l ^ 16) and folded with one shuffle.
+//
+// Phases: (0) problem -> smem with coalesced loads, independent of the
+// previous kernel (overlaps it under programmatic dependent launch);
+// (1) wait for the producer, elite carry-over and breeding; (2) B at the
+// knots and the knot-space input cost; (3) the horizon recursion.
+
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a) {
   constexpr int NRG = NP / RR;
+  constexpr int VEC = Geo<S>::VEC;
+  constexpr int NPS = Geo<S>::nps(NP);
+  constexpr int NSPLIT = (RR * CC >= 8) ? 1 : ((RR * CC >= 4) ? 2 : 4);
+  constexpr int NJ = NP / VEC / KS;  // 16-byte column groups per reduction half
+  constexpr int NPH = NP / KS;       // columns per reduction half
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Dims& d = a.d;
+  const StageLayout& SL = a.SL;
   const int n = d.n, m = d.m, T = d.T, p = d.p, pm = d.pm;
-  const int tileP = a.tileP, pmS = a.pmS;
+  const int tileP = a.tileP, tPS = a.tPS;
   const int inst = blockIdx.y;
   const int tile0 = blockIdx.x * a.tile;
   const int cnt = min(a.tile, a.nc - tile0);
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const S* __restrict__ W = a.work + (size_t)inst * a.L.stride;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthr + 31) >> 5;
+  const double* __restrict__ P = a.prob + (size_t)inst * SL.stride;
+  const double* __restrict__ X = a.state + (size_t)inst * SL.sstride;
 
-  const SmemPlan sp = smem_plan<S>(NP, n, m, T, p, tileP, pmS, AREG, DQ);
+  const SmemPlan sp = smem_plan<S>(NP, m, T, p, tileP, tPS, AREG, DQ);
   unsigned char* ptr = smem_raw;
-  S* Us = reinterpret_cast<S*>(ptr); ptr += sp.us;
-  S* BUT = reinterpret_cast<S*>(ptr); ptr += sp.but;
-  S* XT = reinterpret_cast<S*>(ptr); ptr += sp.xt;
-  S* Dt = reinterpret_cast<S*>(ptr); ptr += sp.dt;
-  S* Qt = reinterpret_cast<S*>(ptr); ptr += sp.qt;
+  S* UsT = reinterpret_cast<S*>(ptr); ptr += sp.us;   // [gene][tPS]
+  S* BUT = reinterpret_cast<S*>(ptr); ptr += sp.but;  // [knot][row][tPS]
+  S* XC = reinterpret_cast<S*>(ptr); ptr += sp.xc;    // [2][tileP][NPS]; Bs [NP][m+1] in the prologue
+  S* As = reinterpret_cast<S*>(ptr); ptr += sp.as;    // [NP][NPS]
+  S* Qs = reinterpret_cast<S*>(ptr); ptr += sp.qs;    // [NP][NPS]
   int* sI1 = reinterpret_cast<int*>(ptr);
   int* sI2 = sI1 + T;
   S* sC = reinterpret_cast<S*>(sI2 + T); ptr += sp.sched;
-  S* sG = reinterpret_cast<S*>(ptr); ptr += sp.g;
+  S* sG = reinterpret_cast<S*>(ptr); ptr += sp.g;     // [p*p] + cost0
   S* cU = reinterpret_cast<S*>(ptr); ptr += sp.cu;
-  int* src = reinterpret_cast<int*>(ptr);
+  int* src = reinterpret_cast<int*>(ptr); ptr += sp.src;
+  S* cw_ = reinterpret_cast<S*>(ptr);                 // w, qd, xg, x0 [NP]; ug, umin, umax, sig, rdiag [m]
+  S* cqd = cw_ + NP;
+  S* cxg = cqd + NP;
+  S* cx0 = cxg + NP;
+  S* cug = cx0 + NP;
+  S* cumin = cug + m;
+  S* cumax = cumin + m;
+  S* csig = cumax + m;
+  S* crd = csig + m;
+  S* Bs = XC;
 
   const size_t pop_base = (size_t)inst * a.rows;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
+
+  EMPC_MARK(0)
+  // ---- phase 0: problem -> smem (coalesced, all loads in flight together)
+  if (cnt > 0) {
+    for (int k = tid; k < T; k += nthr) {
+      sI1[k] = a.idx1[k];
+      sI2[k] = a.idx2[k];
+      sC[k] = a.cw[k];
+    }
+    for (int e = tid; e < p * p; e += nthr) sG[e] = a.G[e];
+    for (int e = tid; e < NP * NP; e += nthr) {
+      const int i = e / NP, j = e - (e / NP) * NP;
+      As[i * NPS + j] = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
+      if constexpr (DQ) Qs[i * NPS + j] = (i < n && j < n) ? (S)P[SL.q + i * n + j] : S(0);
+    }
+    for (int e = tid; e < NP * m; e += nthr) {
+      const int i = e / m, l = e - (e / m) * m;
+      Bs[i * (m + 1) + l] = i < n ? (S)P[SL.bd + i * m + l] : S(0);
+    }
+    for (int i = tid; i < NP; i += nthr) {
+      const bool ok = i < n;
+      cw_[i] = ok ? (S)P[SL.wd + i] : S(0);
+      cqd[i] = ok ? (S)P[SL.q + i * n + i] : S(0);
+      cxg[i] = ok ? (S)P[SL.xg + i] : S(0);
+      cx0[i] = ok ? (S)X[SL.x0 + i] : S(0);
+    }
+    for (int l = tid; l < m; l += nthr) {
+      cug[l] = (S)P[SL.ug + l];
+      cumin[l] = (S)P[SL.umin + l];
+      cumax[l] = (S)P[SL.umax + l];
+      csig[l] = (S)X[SL.sig + l];
+      crd[l] = (S)P[SL.r + l * m + l];
+    }
+    // cost of x_0 (k = 0 state term, K/empc.py:113-118), FP64, warp 0
+    if (warp == 0) {
+      double part = 0.0;
+      for (int i = lane; i < n; i += 32) {
+        const double ei = X[SL.x0 + i] - P[SL.xg + i];
+        if constexpr (DQ) {
+          double qe = 0.0;
+          for (int j = 0; j < n; ++j) qe = fma(P[SL.q + i * n + j], X[SL.x0 + j] - P[SL.xg + j], qe);
+          part = fma(ei, qe, part);
+        } else {
+          part = fma(P[SL.q + i * n + i] * ei, ei, part);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, off);
+      if (lane == 0) sG[p * p] = (S)part;
+    }
+  }
+
+  EMPC_MARK(1)
+  // ---- phase 1: everything below reads the producer grid's outputs
+  pdl_wait();
+  EMPC_MARK(2)
   const RunParams rp = *a.run;
   const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
   const uint32_t gen = (uint32_t)(rp.gen0 + a.evolve);
-
-  // ---- elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
-  // population are the sorted elites with their carried costs.  Spread over
-  // the instance's CTAs.
+  // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
+  // population are the sorted elites with their carried costs.
   if (breed) {
     for (int e = blockIdx.x; e < d.K; e += gridDim.x) {
       const int s = a.elite_idx[(size_t)inst * d.K + e];
@@ -205,15 +258,6 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
     }
   }
   if (cnt <= 0) return;
-
-  for (int k = tid; k < T; k += nthr) {
-    sI1[k] = a.idx1[k];
-    sI2[k] = a.idx2[k];
-    sC[k] = a.cw[k];
-  }
-  for (int e = tid; e < p * p; e += nthr) sG[e] = a.G[e];
-
-  // ---- candidate knots into smem (K5 prologue)
   if (breed) {
     // parents (K/empc.py:196): two uniform elite ranks per child
     for (int c = tid; c < cnt; c += nthr) {
@@ -225,14 +269,16 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
         p2 = pp[1];
       } else {
         const U4 r = philox4x32_10(U4{kParentWord, (uint32_t)child, (uint32_t)inst, gen}, key0, key1);
-        p1 = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift, unbiased to 2^-32
+        p1 = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
         p2 = (int)mulhi32(r.y, (uint32_t)d.K);
       }
       src[2 * c] = a.elite_idx[(size_t)inst * d.K + p1];
       src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + p2];
     }
-    __syncthreads();
   }
+  __syncthreads();  // src, phase-0 smem
+  // candidate knots -> UsT[gene][cand] (K5)
+#pragma unroll 4
   for (int e = tid; e < tileP * pm; e += nthr) {
     const int c = e / pm, g = e - (e / pm) * pm;
     S v = S(0);
@@ -243,7 +289,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
         v = a.pop_in[(pop_base + a.row0 + cand) * pm + g];
       } else if (a.mode == kInitPhilox) {
         const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, kInitTag}, key0, key1);
-        const S lo = W[a.L.umin + l], hi = W[a.L.umax + l];
+        const S lo = cumin[l], hi = cumax[l];
         v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high), K/empc.py:170
         v = v > hi ? hi : v;
       } else if (a.mode == kInitInject) {
@@ -252,6 +298,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
         // crossover, mutation, clip (K/empc.py:197-204)
         const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
         bool take, mut;
+        S dz = S(0);
         if (a.mode == kBreedInject) {
           take = a.inj_take[gi] != 0;
           mut = a.inj_mut[gi] != 0;
@@ -259,281 +306,361 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel(const RolloutArgs<S> a) {
           const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, gen}, key0, key1);
           take = (uint64_t)r.x < rp.thr_cross;
           mut = (uint64_t)r.y < rp.thr_mut;
-          if (mut) {
-            const S z = normal_bm<S>(r.z, r.w);
-            v = z * W[a.L.sig + l];
-          }
+          if (mut) dz = normal_bm<S>(r.z, r.w) * csig[l];
         }
         const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
         if (a.mode == kBreedInject) {
-          // reference arithmetic in FP64: child + mutate*noise*sigma
-          const double nz = mut ? a.inj_noise[gi] * a.sig64[(size_t)inst * a.sig64_stride + l] : 0.0;
+          // the reference's FP64 arithmetic: child + mutate*noise*sigma
+          const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
           v = (S)((double)par + nz);
         } else {
-          v = par + v;
+          v = par + dz;
         }
-        const S lo = W[a.L.umin + l], hi = W[a.L.umax + l];
+        const S lo = cumin[l], hi = cumax[l];
         v = v < lo ? lo : (v > hi ? hi : v);
       }
       if (a.mode != kScore) a.pop_out[(pop_base + a.row0 + cand) * pm + g] = v;
     }
-    Us[c * pmS + g] = v;
+    UsT[g * tPS + c] = v;
   }
   __syncthreads();
+  EMPC_MARK(3)
 
-  // ---- B at the knots (+ w), interpolated later: drive = W (x) (U Bd') + wd
-  // (K/empc.py:104-105).  Layout BUT[knot][row][cand].
-  {
-    const S* __restrict__ Bm = W + a.L.bm;
-    const S* __restrict__ wd = W + a.L.wd;
-    const int tot = p * NP * tileP;
-    for (int e = tid; e < tot; e += nthr) {
-      const int c = e % tileP;
-      const int t = e / tileP;
-      const int i = t % NP, j = t / NP;
-      S v = S(0);
-      if (i < n) {
-        v = wd[i];
-        const S* u = Us + c * pmS + j * m;
-        const S* b = Bm + i * m;
-        for (int l = 0; l < m; ++l) v = fma(b[l], u[l], v);
+  // ---- phase 2
+  // logical thread (rg, cg); with KS = 2 the two halves of the j-reduction
+  // of one logical thread are lanes l and l ^ 16 of the same warp
+  const int lt = KS == 1 ? tid : (((tid >> 5) << 4) | (tid & 15));
+  const int ks = KS == 1 ? 0 : ((tid >> 4) & 1);
+  const int rg = lt % NRG, cg = lt / NRG;
+  const bool active = cg * CC < tileP;
+  // padding threads shadow candidate group 0 so that every lane of a warp
+  // takes part in the shuffles; their results are never stored
+  const int c0 = active ? cg * CC : 0;
+  const bool lead = ks == 0;
+  const int jbase = ks * NPH;
+  // B at the knots (+ w), interpolated later: drive = W (x) (U Bd') + wd
+  // (K/empc.py:104-105).  BUT[knot][row][cand].
+  if (active) {
+    for (int j = ks; j < p; j += KS) {
+      S acc[RR][CC];
+#pragma unroll
+      for (int r = 0; r < RR; ++r) {
+        const S w = cw_[rg + r * NRG];
+#pragma unroll
+        for (int q = 0; q < CC; ++q) acc[r][q] = w;
       }
-      BUT[(j * NP + i) * tileP + c] = v;
+#pragma unroll 4
+      for (int l = 0; l < m; ++l) {
+        S u[CC];
+        lds_vec<S, CC>(UsT + (j * m + l) * tPS + c0, u);
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const S b = Bs[(rg + r * NRG) * (m + 1) + l];
+#pragma unroll
+          for (int q = 0; q < CC; ++q) acc[r][q] = fma(b, u[q], acc[r][q]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) sts_vec<S, CC>(BUT + (j * NP + rg + r * NRG) * tPS + c0, acc[r]);
     }
   }
-  // ---- input cost as the knot quadratic z'(W'W (x) R)z, z = U - u_goal
-  // (K/empc.py:100-101); per (candidate, channel) partials in XT scratch.
-  {
-    S* ru = XT;
-    const S* __restrict__ R = W + a.L.r;
-    const S* __restrict__ ug = W + a.L.ug;
-    for (int e = tid; e < tileP * m; e += nthr) {
-      const int c = e / m, l = e - (e / m) * m;
-      S val = S(0);
-      if (c < cnt) {
-        const S* u = Us + c * pmS;
-        if (p <= 8) {
-          S gz[8];
+  // input cost as the knot quadratic z'(W'W (x) R)z, z = U - u_goal
+  // (K/empc.py:100-101): one warp per candidate, lanes over channels
+  for (int c = warp; c < cnt; c += nwarps) {
+    S val = S(0);
+    for (int l = lane; l < m; l += 32) {
+      const S ugl = cug[l];
+      S gz[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) gz[q] = S(0);
-          for (int b = 0; b < p; ++b) {
-            S rz = S(0);
-            for (int l2 = 0; l2 < m; ++l2) rz = fma(R[l * m + l2], u[b * m + l2] - ug[l2], rz);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (q < p) gz[q] = fma(sG[q * p + b], rz, gz[q]);
+      for (int q = 0; q < 8; ++q) gz[q] = S(0);
+      if (p <= 8) {
+        for (int b = 0; b < p; ++b) {
+          S rz;
+          if (a.r_diag) {
+            rz = crd[l] * (UsT[(b * m + l) * tPS + c] - ugl);
+          } else {
+            rz = S(0);
+            for (int l2 = 0; l2 < m; ++l2)
+              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            if (q < p) val = fma(u[q * m + l] - ug[l], gz[q], val);
-        } else {
-          for (int q = 0; q < p; ++q) {
-            S gzq = S(0);
-            for (int b = 0; b < p; ++b) {
-              S rz = S(0);
-              for (int l2 = 0; l2 < m; ++l2) rz = fma(R[l * m + l2], u[b * m + l2] - ug[l2], rz);
-              gzq = fma(sG[q * p + b], rz, gzq);
-            }
-            val = fma(u[q * m + l] - ug[l], gzq, val);
+            if (q < p) gz[q] = fma(sG[q * p + b], rz, gz[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p) val = fma(UsT[(q * m + l) * tPS + c] - ugl, gz[q], val);
+      } else {
+        for (int q = 0; q < p; ++q) {
+          S gzq = S(0);
+          for (int b = 0; b < p; ++b) {
+            S rz = S(0);
+            for (int l2 = 0; l2 < m; ++l2)
+              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
+            gzq = fma(sG[q * p + b], rz, gzq);
           }
+          val = fma(UsT[(q * m + l) * tPS + c] - ugl, gzq, val);
         }
       }
-      ru[e] = val;
     }
-    __syncthreads();
-    for (int c = tid; c < tileP; c += nthr) {
-      S s = S(0);
-      for (int l = 0; l < m; ++l) s += ru[c * m + l];
-      cU[c] = s;
-    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, off);
+    if (lane == 0) cU[c] = val;
   }
-  // ---- model into registers / smem (A as Delta = Ad - I)
-  const int rg = tid % NRG, cg = tid / NRG;
-  const bool active = cg * CC < tileP;
-  S areg[AREG ? RR : 1][AREG ? NP : 1];
+  // model rows: A (Delta = Ad - I) from smem into registers
+  S areg[AREG ? RR : 1][AREG ? NPH : 1];
   if constexpr (AREG) {
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      const int row = rg * RR + r;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) areg[r][j] = (row < n && j < n) ? W[a.L.dm + row * n + j] : S(0);
-    }
-  } else {
-    for (int e = tid; e < NP * NP; e += nthr) {
-      const int j = e / NP, i = e % NP;
-      Dt[e] = (i < n && j < n) ? W[a.L.dm + i * n + j] : S(0);
-      if constexpr (DQ) Qt[e] = (i < n && j < n) ? W[a.L.qf + i * n + j] : S(0);
-    }
-  }
-  S qv[RR], xgv[RR], qxg[RR];
-#pragma unroll
-  for (int r = 0; r < RR; ++r) {
-    const int row = rg * RR + r;
-    qv[r] = (row < n && !DQ) ? W[a.L.qd + row] : S(0);
-    xgv[r] = row < n ? W[a.L.xg + row] : S(0);
-    qxg[r] = (row < n && DQ) ? W[a.L.qxg + row] : S(0);
-  }
-  __syncthreads();  // ru (in XT) consumed; Dt/Qt/BUT visible
-  // x_0 = x0 for every candidate (K/empc.py:109)
-  for (int e = tid; e < NP * tileP; e += nthr) {
-    const int i = e / tileP;
-    XT[e] = i < n ? W[a.L.x0 + i] : S(0);
-  }
-  S xo[RR][CC];
-#pragma unroll
-  for (int r = 0; r < RR; ++r) {
-    const int row = rg * RR + r;
-    const S x0r = row < n ? W[a.L.x0 + row] : S(0);
-#pragma unroll
-    for (int c = 0; c < CC; ++c) xo[r][c] = x0r;
-  }
-  S cst[CC];
-#pragma unroll
-  for (int c = 0; c < CC; ++c) cst[c] = S(0);
-  __syncthreads();
-
-  // ---- horizon recursion x_{k+1} = x_k + Delta x_k + drive_k
-  // (K/empc.py:110-112), state cost fused per step (K/empc.py:113-118)
-  const int col = cg * CC;
-  for (int k = 0; k < T; ++k) {
-    const S* xc = XT + (k & 1) * NP * tileP;
-    S* xnb = XT + ((k & 1) ^ 1) * NP * tileP;
-    S acc[RR][CC];
-    S qacc[DQ ? RR : 1][DQ ? CC : 1];
 #pragma unroll
     for (int r = 0; r < RR; ++r)
 #pragma unroll
-      for (int c = 0; c < CC; ++c) acc[r][c] = S(0);
-    if constexpr (DQ) {
+      for (int jv = 0; jv < NPH / VEC; ++jv) {
+        S t[VEC];
+        lds_vec<S, VEC>(As + (rg + r * NRG) * NPS + jbase + jv * VEC, t);
 #pragma unroll
-      for (int r = 0; r < RR; ++r)
-#pragma unroll
-        for (int c = 0; c < CC; ++c) qacc[r][c] = S(0);
-    }
-    if (active) {
-#pragma unroll(AREG ? NP : 16)
-      for (int j = 0; j < NP; ++j) {
-        S xv[CC];
-        lds_vec<S, CC>(xc + j * tileP + col, xv);
-        S av[RR];
-        if constexpr (AREG) {
-#pragma unroll
-          for (int r = 0; r < RR; ++r) av[r] = areg[r][j];
-        } else {
-          lds_vec<S, RR>(Dt + j * NP + rg * RR, av);
-        }
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int c = 0; c < CC; ++c) acc[r][c] = fma(av[r], xv[c], acc[r][c]);
-        if constexpr (DQ) {
-          S qa[RR];
-          lds_vec<S, RR>(Qt + j * NP + rg * RR, qa);
-#pragma unroll
-          for (int r = 0; r < RR; ++r)
-#pragma unroll
-            for (int c = 0; c < CC; ++c) qacc[r][c] = fma(qa[r], xv[c], qacc[r][c]);
-        }
+        for (int q = 0; q < VEC; ++q) areg[r][jv * VEC + q] = t[q];
       }
-      const int i1 = sI1[k], i2 = sI2[k];
-      const S ck = sC[k], c1 = S(1) - ck;
+  }
+  S qv[RR], xgv[RR], qxg[RR], xo[RR][CC];
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const int row = rg + r * NRG;
+    qv[r] = DQ ? S(0) : cqd[row];
+    xgv[r] = cxg[row];
+    qxg[r] = S(0);
+    if constexpr (DQ) {
+      if (row < n) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s = fma(P[SL.q + row * n + j], P[SL.xg + j], s);
+        qxg[r] = (S)s;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CC; ++q) xo[r][q] = cx0[row];
+  }
+  S cst[CC];
+#pragma unroll
+  for (int q = 0; q < CC; ++q) cst[q] = S(0);
+  __syncthreads();  // Bs (in XC) consumed; BUT / cU visible
+  // x_0 = x0 for every candidate (K/empc.py:109)
+  for (int e = tid; e < tileP * NPS; e += nthr) {
+    const int i = e % NPS;
+    XC[e] = i < NP ? cx0[i] : S(0);
+  }
+  __syncthreads();
+  // the next kernel may start its independent prologue now
+  pdl_trigger();
+  EMPC_MARK(4)
+
+  // partial products of the rows with this thread's column half, with
+  // software-pipelined 16-byte loads (the next column group is in flight
+  // while the current one is consumed); KS == 2 folds the halves with one
+  // shuffle.  A macro, not a lambda, so the register arrays stay in registers.
+#define EMPC_MATVEC(FROMREG, MS, XB, OUT)                                                             \
+  {                                                                                                   \
+    S part_[RR][CC][NSPLIT];                                                                          \
+    _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
+    _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                    \
+    _Pragma("unroll") for (int s = 0; s < NSPLIT; ++s) part_[r][q][s] = S(0);                         \
+    S xv_[2][CC][VEC];                                                                                \
+    _Pragma("unroll") for (int q = 0; q < CC; ++q) lds_vec<S, VEC>((XB) + q * NPS + jbase, xv_[0][q]); \
+    _Pragma("unroll") for (int jj = 0; jj < NJ; ++jj) {                                               \
+      if (jj + 1 < NJ) {                                                                              \
+        _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                \
+          lds_vec<S, VEC>((XB) + q * NPS + jbase + (jj + 1) * VEC, xv_[(jj + 1) & 1][q]);             \
+      }                                                                                               \
+      S av_[RR][VEC];                                                                                 \
+      _Pragma("unroll") for (int r = 0; r < RR; ++r) {                                                \
+        if constexpr (FROMREG) {                                                                      \
+          _Pragma("unroll") for (int t = 0; t < VEC; ++t) av_[r][t] = areg[r][AREG ? jj * VEC + t : 0]; \
+        } else {                                                                                      \
+          lds_vec<S, VEC>((MS) + (rg + r * NRG) * NPS + jbase + jj * VEC, av_[r]);                    \
+        }                                                                                             \
+      }                                                                                               \
+      _Pragma("unroll") for (int t = 0; t < VEC; ++t)                                                 \
+      _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                  \
+      _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                  \
+        part_[r][q][t % NSPLIT] = fma(av_[r][t], xv_[jj & 1][q][t], part_[r][q][t % NSPLIT]);         \
+    }                                                                                                 \
+    _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
+    _Pragma("unroll") for (int q = 0; q < CC; ++q) {                                                  \
+      S t_ = part_[r][q][0];                                                                          \
+      _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) t_ += part_[r][q][s];                        \
+      if constexpr (KS == 2) t_ += __shfl_xor_sync(0xFFFFFFFFu, t_, 16);                              \
+      (OUT)[r][q] = t_;                                                                               \
+    }                                                                                                 \
+  }
+
+  // ---- phase 3: horizon recursion x_{k+1} = x_k + Delta x_k + drive_k
+  // (K/empc.py:110-112), state cost fused per step (K/empc.py:113-118).
+  // The knot pair of the drive changes p - 1 times over the horizon: the
+  // interpolation endpoints B U_j + w are cached in registers.
+  int ci1 = -1, ci2 = -1;
+  S b1[RR][CC], b2[RR][CC];
+  for (int k = 0; k < T; ++k) {
+    const S* xb = XC + (k & 1) * tileP * NPS + c0 * NPS;
+    S* xw = XC + ((k & 1) ^ 1) * tileP * NPS;
+    S ax[RR][CC];
+    EMPC_MATVEC(AREG, As, xb, ax)
+    S qx[DQ ? RR : 1][DQ ? CC : 1];
+    if constexpr (DQ) EMPC_MATVEC(false, Qs, xb, qx)
+    const int i1 = sI1[k], i2 = sI2[k];
+    const S ck = sC[k], c1 = S(1) - ck;
+    if (i1 != ci1 || i2 != ci2) {  // uniform across the CTA
+      ci1 = i1;
+      ci2 = i2;
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
-        const int row = rg * RR + r;
-        S b1[CC], b2[CC];
-        lds_vec<S, CC>(BUT + (i1 * NP + row) * tileP + col, b1);
-        lds_vec<S, CC>(BUT + (i2 * NP + row) * tileP + col, b2);
-        S xn[CC];
+        lds_vec<S, CC>(BUT + (i1 * NP + rg + r * NRG) * tPS + c0, b1[r]);
+        lds_vec<S, CC>(BUT + (i2 * NP + rg + r * NRG) * tPS + c0, b2[r]);
+      }
+    }
 #pragma unroll
-        for (int c = 0; c < CC; ++c) {
-          if constexpr (DQ) {
-            const S e0 = xo[r][c] - xgv[r];
-            cst[c] = fma(e0, qacc[r][c] - qxg[r], cst[c]);  // cost of x_k
-          }
-          const S drive = fma(ck, b2[c], c1 * b1[c]);
-          xn[c] = xo[r][c] + (acc[r][c] + drive);
-          xo[r][c] = xn[c];
-          if constexpr (!DQ) {
-            const S e = xn[c] - xgv[r];
-            cst[c] = fma(qv[r] * e, e, cst[c]);  // cost of x_{k+1}, diagonal Q
-          }
+    for (int r = 0; r < RR; ++r) {
+      const int row = rg + r * NRG;
+#pragma unroll
+      for (int q = 0; q < CC; ++q) {
+        if constexpr (DQ) cst[q] = fma(xo[r][q] - xgv[r], qx[r][q] - qxg[r], cst[q]);  // cost of x_k
+        const S drive = fma(ck, b2[r][q], c1 * b1[r][q]);
+        const S xn = xo[r][q] + (ax[r][q] + drive);
+        xo[r][q] = xn;
+        if constexpr (!DQ) {
+          const S e = xn - xgv[r];
+          cst[q] = fma(qv[r] * e, e, cst[q]);  // cost of x_{k+1}, diagonal Q
         }
-        sts_vec<S, CC>(xnb + row * tileP + col, xn);
+        if (lead && active) xw[(c0 + q) * NPS + row] = xn;
       }
     }
     __syncthreads();
   }
   if constexpr (DQ) {
     // terminal state term e_T' Q e_T
-    if (active) {
-      const S* xc = XT + (T & 1) * NP * tileP;
-      S qacc[RR][CC];
+    const S* xb = XC + (T & 1) * tileP * NPS + c0 * NPS;
+    S qf[RR][CC];
+    EMPC_MATVEC(false, Qs, xb, qf)
 #pragma unroll
-      for (int r = 0; r < RR; ++r)
+    for (int r = 0; r < RR; ++r)
 #pragma unroll
-        for (int c = 0; c < CC; ++c) qacc[r][c] = S(0);
-#pragma unroll 8
-      for (int j = 0; j < NP; ++j) {
-        S xv[CC], qa[RR];
-        lds_vec<S, CC>(xc + j * tileP + col, xv);
-        lds_vec<S, RR>(Qt + j * NP + rg * RR, qa);
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int c = 0; c < CC; ++c) qacc[r][c] = fma(qa[r], xv[c], qacc[r][c]);
-      }
-#pragma unroll
-      for (int r = 0; r < RR; ++r)
-#pragma unroll
-        for (int c = 0; c < CC; ++c) cst[c] = fma(xo[r][c] - xgv[r], qacc[r][c] - qxg[r], cst[c]);
-    }
+      for (int q = 0; q < CC; ++q) cst[q] = fma(xo[r][q] - xgv[r], qf[r][q] - qxg[r], cst[q]);
   }
+  EMPC_MARK(5)
   // ---- deterministic reduction over row groups (BUT is free now)
   S* red = BUT;
-  if (active) {
+  if (active && lead) {
 #pragma unroll
-    for (int c = 0; c < CC; ++c) red[rg * tileP + col + c] = cst[c];
+    for (int q = 0; q < CC; ++q) red[rg * tPS + c0 + q] = cst[q];
   }
   __syncthreads();
-  const S c0 = DQ ? S(0) : W[a.L.cost0];
+  const S c0s = DQ ? S(0) : sG[p * p];
+  // children whose key beats the K-th elite's are appended to the instance's
+  // qualifier list (order is irrelevant: keys are unique and get sorted)
+  using OT = typename std::conditional<sizeof(S) == 4, uint32_t, uint64_t>::type;
+  OT tau = OT(0);
+  const bool qual = breed && a.qcount != nullptr;
+  if (qual) tau = ord_key(a.cost_in[pop_base + a.elite_idx[(size_t)inst * d.K + d.K - 1]]);
   for (int c = tid; c < cnt; c += nthr) {
     S s = S(0);
-    for (int g = 0; g < NRG; ++g) s += red[g * tileP + c];
-    a.cost_out[pop_base + a.row0 + tile0 + c] = c0 + cU[c] + s;
+    for (int g = 0; g < NRG; ++g) s += red[g * tPS + c];
+    const S cost = c0s + cU[c] + s;
+    const int row = a.row0 + tile0 + c;
+    a.cost_out[pop_base + row] = cost;
+    if (qual) {
+      const OT kc = ord_key(cost);
+      if (kc < tau) {
+        const int slot = atomicAdd(a.qcount + inst, 1);
+        if (slot < a.qcap) {
+          OT* ql = reinterpret_cast<OT*>(a.qlist) + (size_t)inst * a.qcap * 2;
+          ql[2 * slot] = kc;
+          ql[2 * slot + 1] = (OT)row;
+        }
+      }
+    }
   }
+  EMPC_MARK(6)
+#undef EMPC_MATVEC
 }
 
 // ---------------------------------------------------------------------------
-// K4 selection: bitonic sort of (cost, index) keys in shared memory, one CTA
-// per instance; rows [0, K) of the sorted order are the elites.
+// K4 selection: stable top-K (argsort(kind="stable")[:K], K/empc.py:185-186).
+// Key of candidate i = (ord(cost_i), i) -- unique, so the stable order is the
+// key order and the result is deterministic.  Rank by counting, spread over
+// the whole GPU: every CTA loads the instance's candidate keys into shared
+// memory and ranks a slice of them (one warp per candidate, lanes over the
+// set); a candidate of rank r < K lands in elite slot r.
+//
+// Candidate set: all N rows for the first selection of a run.  After an
+// evolve, rows [0, K) hold the previous elites and only children that beat
+// the K-th of them (appended to a qualifier list by the rollout epilogue) can
+// enter: every other key is larger than every key of this set, so ranks
+// within the set are global ranks.  The qualifier lists are double-buffered
+// by evolve parity; the selection resets the list the next rollout fills.
 
 template <typename S>
-__global__ void __launch_bounds__(1024) select_kernel(const S* __restrict__ costs, int N, int K, int NP2,
-                                                      int* __restrict__ elite_idx) {
-  using KT = typename KeyOf<S>::type;
+struct OrdOf;
+template <>
+struct OrdOf<float> {
+  using T = uint32_t;
+  __device__ __forceinline__ static T ord(float c) { return ord32(c); }
+};
+template <>
+struct OrdOf<double> {
+  using T = uint64_t;
+  __device__ __forceinline__ static T ord(double c) { return ord64(c); }
+};
+
+template <typename S>
+__host__ __device__ inline size_t select_smem(int N) {
+  using OT = typename std::conditional<sizeof(S) == 4, uint32_t, uint64_t>::type;
+  return (size_t)N * (sizeof(OT) + sizeof(int));
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs, int N, int K,
+                                                     int* __restrict__ elite_idx, int incremental,
+                                                     int* __restrict__ qcount_in, const void* __restrict__ qlist_in,
+                                                     int* __restrict__ qcount_next, int qcap) {
+  using OT = typename OrdOf<S>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  KT* keys = reinterpret_cast<KT*>(smem_raw);
-  const int inst = blockIdx.x;
+  OT* ck = reinterpret_cast<OT*>(smem_raw);
+  int* ci = reinterpret_cast<int*>(ck + N);
+  const int inst = blockIdx.y;
   const S* c = costs + (size_t)inst * N;
-  for (int i = threadIdx.x; i < NP2; i += blockDim.x) keys[i] = i < N ? KeyOf<S>::make(c[i], i) : KeyOf<S>::pad();
-  __syncthreads();
-  const int half = NP2 >> 1;
-  for (int k = 2; k <= NP2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < half; t += blockDim.x) {
-        const int lo = 2 * j * (t / j) + (t % j);
-        const int hi = lo + j;
-        const bool asc = (lo & k) == 0;
-        const KT a = keys[lo], b = keys[hi];
-        if ((b < a) == asc) {
-          keys[lo] = b;
-          keys[hi] = a;
-        }
-      }
-      __syncthreads();
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  pdl_wait();     // costs come from the previous rollout
+  int L = 0;
+  bool full = !incremental || K >= N || qcount_in == nullptr;
+  if (!full) {
+    L = qcount_in[inst];
+    full = L > qcap || K + L > N;
+  }
+  __syncthreads();  // all reads of the count precede its reset below
+  if (blockIdx.x == 0 && tid == 0 && qcount_next != nullptr) qcount_next[inst] = 0;
+  pdl_trigger();  // the next rollout may start its independent prologue
+  const int M = full ? N : K + L;
+  const OT* ql = full ? nullptr : reinterpret_cast<const OT*>(qlist_in) + (size_t)inst * qcap * 2;
+  for (int j = tid; j < M; j += nthr) {
+    if (j < K || full) {
+      ck[j] = OrdOf<S>::ord(c[j]);
+      ci[j] = j;
+    } else {
+      ck[j] = ql[2 * (j - K)];
+      ci[j] = (int)ql[2 * (j - K) + 1];
     }
   }
-  for (int e = threadIdx.x; e < K; e += blockDim.x) elite_idx[(size_t)inst * K + e] = keys[e].idx();
+  __syncthreads();
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int e0 = blockIdx.x * per, e1 = min(M, e0 + per);
+  for (int e = e0 + warp; e < e1; e += nwarps) {
+    const OT ke = ck[e];
+    const int re = ci[e];
+    int cnt = 0;
+    for (int j = lane; j < M; j += 32) {
+      const OT kj = ck[j];
+      cnt += (kj < ke || (kj == ke && ci[j] < re)) ? 1 : 0;
+    }
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (lane == 0 && cnt < K) elite_idx[(size_t)inst * K + cnt] = re;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -545,6 +672,7 @@ __global__ void finalize_kernel(const S* __restrict__ cands, const S* __restrict
                                 double* __restrict__ out) {
   const int inst = blockIdx.x;
   const S* c = costs + (size_t)inst * N;
+  pdl_wait();
   uint64_t bo = ~0ull;
   int bi = 0x7FFFFFFF;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -618,6 +746,7 @@ __global__ void uncast_kernel(const S* __restrict__ in, double* __restrict__ out
     out[i] = (double)in[i];
 }
 
+#ifdef EMPC_HOST_TU
 // L2 flush for timing hygiene (writes a buffer larger than the 126 MB L2)
 __global__ void flush_kernel(uint4* buf, size_t n, uint32_t v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -630,5 +759,7 @@ __global__ void philox_kernel(const uint32_t* ctr, const uint32_t* key, int coun
   const U4 r = philox4x32_10(U4{ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]}, key[2 * i], key[2 * i + 1]);
   out[4 * i] = r.x; out[4 * i + 1] = r.y; out[4 * i + 2] = r.z; out[4 * i + 3] = r.w;
 }
+
+#endif  // EMPC_HOST_TU
 
 }  // namespace empc

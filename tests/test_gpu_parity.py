@@ -104,10 +104,6 @@ def _select(costs, K, precision="fp32"):
 @pytest.mark.parametrize("N,K", [(1, 1), (2, 1), (8, 8), (100, 6), (1024, 64), (4096, 256), (5000, 77), (16384, 1024)])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_selection_bit_exact(N, K, precision):
-    if precision == "fp64" and N > 8192:
-        with pytest.raises(ValueError):
-            _select(np.zeros(N), K, precision)
-        return
     rng = np.random.default_rng(N + K)
     costs = rng.normal(size=N).astype(np.float32).astype(np.float64)
     # ties, duplicates, signed zeros, infinities
