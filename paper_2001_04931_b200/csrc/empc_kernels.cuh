@@ -111,7 +111,7 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.g = al((size_t)(p * p + 2) * sizeof(S));
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
-  s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S));
+  s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S) + (size_t)((tileP * p * m + 31) / 32 + 1) * 4);
   s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv;
   return s;
 }
@@ -239,13 +239,62 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
     }
   }
 
-  EMPC_MARK(1)
-  // ---- phase 1: everything below reads the producer grid's outputs
-  pdl_wait();
-  EMPC_MARK(2)
+  __syncthreads();  // phase-0 smem (bounds, sigma) is read by every thread below
+  // ---- phase 1a: random draws -- counter-based, so also independent of the
+  // producer grid (the run parameters are staged by the host copy)
   const RunParams rp = *a.run;
   const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
   const uint32_t gen = (uint32_t)(rp.gen0 + a.evolve);
+  uint32_t* tbits = reinterpret_cast<uint32_t*>(cw_ + 4 * NP + 5 * m);  // crossover bits, 1 per gene
+  const bool philox_breed = a.mode == kBreedPhilox;
+  if (cnt > 0) {
+    if (breed) {
+      // parents (K/empc.py:196): two uniform elite ranks per child
+      for (int c = tid; c < cnt; c += nthr) {
+        const int child = tile0 + c;
+        if (a.mode == kBreedInject) {
+          const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
+          src[2 * c] = pp[0];
+          src[2 * c + 1] = pp[1];
+        } else {
+          const U4 r = philox4x32_10(U4{kParentWord, (uint32_t)child, (uint32_t)inst, gen}, key0, key1);
+          src[2 * c] = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
+          src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)d.K);
+        }
+      }
+    }
+    if (philox_breed || a.mode == kInitPhilox) {
+      // crossover bit + mutation offset (K/empc.py:197-199), or the uniform
+      // initial knot (K/empc.py:170), per gene into UsT
+      for (int e0 = 0; e0 < tileP * pm; e0 += nthr) {
+        const int e = e0 + tid;
+        const int c = e / pm, g = e - (e / pm) * pm;
+        bool take = false;
+        if (e < tileP * pm && c < cnt) {
+          const int l = g % m;
+          const int cand = tile0 + c;
+          if (philox_breed) {
+            const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, gen}, key0, key1);
+            take = (uint64_t)r.x < rp.thr_cross;
+            const bool mut = (uint64_t)r.y < rp.thr_mut;
+            UsT[g * tPS + c] = mut ? normal_bm<S>(r.z, r.w) * csig[l] : S(0);
+          } else {
+            const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, kInitTag}, key0, key1);
+            const S lo = cumin[l], hi = cumax[l];
+            const S v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
+            UsT[g * tPS + c] = v > hi ? hi : v;
+          }
+        }
+        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, take);
+        if (lane == 0 && e0 + warp * 32 < tileP * pm) tbits[(e0 + warp * 32) >> 5] = bits;
+      }
+    }
+  }
+
+  EMPC_MARK(1)
+  // ---- phase 1b: everything below reads the producer grid's outputs
+  pdl_wait();
+  EMPC_MARK(2)
   // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
   // population are the sorted elites with their carried costs.
   if (breed) {
@@ -259,25 +308,13 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   }
   if (cnt <= 0) return;
   if (breed) {
-    // parents (K/empc.py:196): two uniform elite ranks per child
-    for (int c = tid; c < cnt; c += nthr) {
-      const int child = tile0 + c;
-      int p1, p2;
-      if (a.mode == kBreedInject) {
-        const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
-        p1 = pp[0];
-        p2 = pp[1];
-      } else {
-        const U4 r = philox4x32_10(U4{kParentWord, (uint32_t)child, (uint32_t)inst, gen}, key0, key1);
-        p1 = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
-        p2 = (int)mulhi32(r.y, (uint32_t)d.K);
-      }
-      src[2 * c] = a.elite_idx[(size_t)inst * d.K + p1];
-      src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + p2];
+    for (int c = tid; c < cnt; c += nthr) {  // elite ranks -> population rows
+      src[2 * c] = a.elite_idx[(size_t)inst * d.K + src[2 * c]];
+      src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + src[2 * c + 1]];
     }
   }
-  __syncthreads();  // src, phase-0 smem
-  // candidate knots -> UsT[gene][cand] (K5)
+  __syncthreads();  // src, phase-0/1a smem
+  // candidate knots -> UsT[gene][cand] (+ the population rows)
 #pragma unroll 4
   for (int e = tid; e < tileP * pm; e += nthr) {
     const int c = e / pm, g = e - (e / pm) * pm;
@@ -288,34 +325,23 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       if (a.mode == kScore) {
         v = a.pop_in[(pop_base + a.row0 + cand) * pm + g];
       } else if (a.mode == kInitPhilox) {
-        const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, kInitTag}, key0, key1);
-        const S lo = cumin[l], hi = cumax[l];
-        v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high), K/empc.py:170
-        v = v > hi ? hi : v;
+        v = UsT[g * tPS + c];
       } else if (a.mode == kInitInject) {
         v = a.inj_init[((size_t)inst * a.nc + cand) * pm + g];
-      } else {
-        // crossover, mutation, clip (K/empc.py:197-204)
-        const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
-        bool take, mut;
-        S dz = S(0);
-        if (a.mode == kBreedInject) {
-          take = a.inj_take[gi] != 0;
-          mut = a.inj_mut[gi] != 0;
-        } else {
-          const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, gen}, key0, key1);
-          take = (uint64_t)r.x < rp.thr_cross;
-          mut = (uint64_t)r.y < rp.thr_mut;
-          if (mut) dz = normal_bm<S>(r.z, r.w) * csig[l];
-        }
+      } else if (philox_breed) {
+        // crossover, mutation, clip (K/empc.py:201-204)
+        const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
         const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
-        if (a.mode == kBreedInject) {
-          // the reference's FP64 arithmetic: child + mutate*noise*sigma
-          const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
-          v = (S)((double)par + nz);
-        } else {
-          v = par + dz;
-        }
+        const S lo = cumin[l], hi = cumax[l];
+        v = par + UsT[g * tPS + c];
+        v = v < lo ? lo : (v > hi ? hi : v);
+      } else {
+        // injected draws, with the reference's FP64 arithmetic child + mutate*noise*sigma
+        const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
+        const bool take = a.inj_take[gi] != 0, mut = a.inj_mut[gi] != 0;
+        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+        const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
+        v = (S)((double)par + nz);
         const S lo = cumin[l], hi = cumax[l];
         v = v < lo ? lo : (v > hi ? hi : v);
       }
@@ -336,8 +362,11 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   // padding threads shadow candidate group 0 so that every lane of a warp
   // takes part in the shuffles; their results are never stored
   const int c0 = active ? cg * CC : 0;
-  const bool lead = ks == 0;
   const int jbase = ks * NPH;
+  // epilogue split: with KS = 2 each lane of the pair finishes half of the
+  // candidates (CH of them, starting at candidate ce)
+  constexpr int CH = KS == 2 ? CC / 2 : CC;
+  const int ce = c0 + ks * CH;
   // B at the knots (+ w), interpolated later: drive = W (x) (U Bd') + wd
   // (K/empc.py:104-105).  BUT[knot][row][cand].
   if (active) {
@@ -420,7 +449,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
         for (int q = 0; q < VEC; ++q) areg[r][jv * VEC + q] = t[q];
       }
   }
-  S qv[RR], xgv[RR], qxg[RR], xo[RR][CC];
+  S qv[RR], xgv[RR], qxg[RR], xo[RR][CH];
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
     const int row = rg + r * NRG;
@@ -435,11 +464,11 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       }
     }
 #pragma unroll
-    for (int q = 0; q < CC; ++q) xo[r][q] = cx0[row];
+    for (int q = 0; q < CH; ++q) xo[r][q] = cx0[row];
   }
-  S cst[CC];
+  S cst[CH];
 #pragma unroll
-  for (int q = 0; q < CC; ++q) cst[q] = S(0);
+  for (int q = 0; q < CH; ++q) cst[q] = S(0);
   __syncthreads();  // Bs (in XC) consumed; BUT / cU visible
   // x_0 = x0 for every candidate (K/empc.py:109)
   for (int e = tid; e < tileP * NPS; e += nthr) {
@@ -481,12 +510,22 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                  \
         part_[r][q][t % NSPLIT] = fma(av_[r][t], xv_[jj & 1][q][t], part_[r][q][t % NSPLIT]);         \
     }                                                                                                 \
+    S sum_[RR][CC];                                                                                   \
     _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
     _Pragma("unroll") for (int q = 0; q < CC; ++q) {                                                  \
-      S t_ = part_[r][q][0];                                                                          \
-      _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) t_ += part_[r][q][s];                        \
-      if constexpr (KS == 2) t_ += __shfl_xor_sync(0xFFFFFFFFu, t_, 16);                              \
-      (OUT)[r][q] = t_;                                                                               \
+      sum_[r][q] = part_[r][q][0];                                                                    \
+      _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) sum_[r][q] += part_[r][q][s];                \
+    }                                                                                                 \
+    _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
+    _Pragma("unroll") for (int q = 0; q < CH; ++q) {                                                  \
+      if constexpr (KS == 2) {                                                                        \
+        /* keep my half, send the partner its half: one shuffle per result */                        \
+        const S mine_ = ks ? sum_[r][CH + q] : sum_[r][q];                                            \
+        const S give_ = ks ? sum_[r][q] : sum_[r][CH + q];                                            \
+        (OUT)[r][q] = mine_ + __shfl_xor_sync(0xFFFFFFFFu, give_, 16);                                \
+      } else {                                                                                        \
+        (OUT)[r][q] = sum_[r][q];                                                                     \
+      }                                                                                               \
     }                                                                                                 \
   }
 
@@ -495,13 +534,13 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   // The knot pair of the drive changes p - 1 times over the horizon: the
   // interpolation endpoints B U_j + w are cached in registers.
   int ci1 = -1, ci2 = -1;
-  S b1[RR][CC], b2[RR][CC];
+  S b1[RR][CH], b2[RR][CH];
   for (int k = 0; k < T; ++k) {
     const S* xb = XC + (k & 1) * tileP * NPS + c0 * NPS;
     S* xw = XC + ((k & 1) ^ 1) * tileP * NPS;
-    S ax[RR][CC];
+    S ax[RR][CH];
     EMPC_MATVEC(AREG, As, xb, ax)
-    S qx[DQ ? RR : 1][DQ ? CC : 1];
+    S qx[DQ ? RR : 1][DQ ? CH : 1];
     if constexpr (DQ) EMPC_MATVEC(false, Qs, xb, qx)
     const int i1 = sI1[k], i2 = sI2[k];
     const S ck = sC[k], c1 = S(1) - ck;
@@ -510,15 +549,15 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       ci2 = i2;
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
-        lds_vec<S, CC>(BUT + (i1 * NP + rg + r * NRG) * tPS + c0, b1[r]);
-        lds_vec<S, CC>(BUT + (i2 * NP + rg + r * NRG) * tPS + c0, b2[r]);
+        lds_vec<S, CH>(BUT + (i1 * NP + rg + r * NRG) * tPS + ce, b1[r]);
+        lds_vec<S, CH>(BUT + (i2 * NP + rg + r * NRG) * tPS + ce, b2[r]);
       }
     }
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
       const int row = rg + r * NRG;
 #pragma unroll
-      for (int q = 0; q < CC; ++q) {
+      for (int q = 0; q < CH; ++q) {
         if constexpr (DQ) cst[q] = fma(xo[r][q] - xgv[r], qx[r][q] - qxg[r], cst[q]);  // cost of x_k
         const S drive = fma(ck, b2[r][q], c1 * b1[r][q]);
         const S xn = xo[r][q] + (ax[r][q] + drive);
@@ -527,7 +566,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
           const S e = xn - xgv[r];
           cst[q] = fma(qv[r] * e, e, cst[q]);  // cost of x_{k+1}, diagonal Q
         }
-        if (lead && active) xw[(c0 + q) * NPS + row] = xn;
+        if (active) xw[(ce + q) * NPS + row] = xn;
       }
     }
     __syncthreads();
@@ -535,19 +574,19 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   if constexpr (DQ) {
     // terminal state term e_T' Q e_T
     const S* xb = XC + (T & 1) * tileP * NPS + c0 * NPS;
-    S qf[RR][CC];
+    S qf[RR][CH];
     EMPC_MATVEC(false, Qs, xb, qf)
 #pragma unroll
     for (int r = 0; r < RR; ++r)
 #pragma unroll
-      for (int q = 0; q < CC; ++q) cst[q] = fma(xo[r][q] - xgv[r], qf[r][q] - qxg[r], cst[q]);
+      for (int q = 0; q < CH; ++q) cst[q] = fma(xo[r][q] - xgv[r], qf[r][q] - qxg[r], cst[q]);
   }
   EMPC_MARK(5)
   // ---- deterministic reduction over row groups (BUT is free now)
   S* red = BUT;
-  if (active && lead) {
+  if (active) {
 #pragma unroll
-    for (int q = 0; q < CC; ++q) red[rg * tPS + c0 + q] = cst[q];
+    for (int q = 0; q < CH; ++q) red[rg * tPS + ce + q] = cst[q];
   }
   __syncthreads();
   const S c0s = DQ ? S(0) : sG[p * p];

@@ -397,25 +397,76 @@ def test_philox_known_answers():
     assert list(got[2]) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
 
 
-def test_philox_operator_statistics():
-    """Mask rates, parent uniformity and mutation noise moments of the
-    in-kernel streams (one generation of a large population)."""
-    spec = _spec()
-    s = P.EmpcSettings(num_sims=16000, num_parents=50, seed=3, sigma_noise=np.array([0.5]), mutation_prob=0.3,
+def _stat_problem(m=4, p=5):
+    model = P.DiscreteLinearModel(np.array([[1.0, 0.02], [-0.4, 0.97]]), np.full((2, m), 0.01), np.zeros(2), 0.02)
+    spec = P.MpcSpec(model, 20, Q=np.diag([10.0, 0.1]), R=0.01 * np.eye(m), x_goal=np.array([0.5, 0.0]),
+                     u_goal=np.zeros(m), u_min=-1e7, u_max=1e7)
+    return spec, P.KnotSchedule(20, p)
+
+
+def test_philox_mutation_statistics():
+    """Mutation rate and noise moments of the in-kernel streams over one
+    generation (~4e5 genes, all elites zero so a child gene is 0 or sigma*z);
+    bounds are 5 sigma."""
+    spec, sched = _stat_problem()
+    N, K = 16000, 50
+    s = P.EmpcSettings(num_sims=N, num_parents=K, seed=3, sigma_noise=np.full(4, 0.5), mutation_prob=0.3,
                        crossover_prob=0.5)
-    # all elites equal except one gene pattern -> children reveal the operators
-    base = np.zeros((16000, 3, 1))
-    costs = np.arange(16000, dtype=float)
-    pop = P.Population(base, costs, 5)
-    x_far = np.array([100.0, 0.0])  # sigma at full scale
-    out = P.evolve_generation(pop, spec, SCHED, s, x_far)
-    kids = out.candidates[50:].ravel()
+    pop = P.Population(np.zeros((N, 5, 4)), np.arange(N, dtype=float), 5)
+    kids = P.evolve_generation(pop, spec, sched, s, np.array([100.0, 0.0])).candidates[K:].ravel()
     mutated = kids != 0.0
-    assert abs(mutated.mean() - 0.3) < 0.01
+    assert abs(mutated.mean() - 0.3) < 5 * np.sqrt(0.3 * 0.7 / kids.size)
     z = kids[mutated] / 0.5
-    assert abs(z.mean()) < 0.02
-    assert abs(z.std() - 1.0) < 0.02
-    assert abs(np.mean(np.abs(z) > 1.96) - 0.05) < 0.01
+    n = z.size
+    assert abs(z.mean()) < 5 / np.sqrt(n)
+    assert abs(z.std() - 1.0) < 5 / np.sqrt(2 * n)
+    assert abs(np.mean(np.abs(z) > 1.96) - 0.05) < 5 * np.sqrt(0.05 * 0.95 / n)
+
+
+def test_philox_parent_and_crossover_statistics():
+    """Parents uniform over the K elites, genes from at most two parents, and
+    a per-gene crossover rate of 1/2 (K/empc.py:196-201)."""
+    spec, sched = _stat_problem()
+    N, K = 16000, 50
+    s = P.EmpcSettings(num_sims=N, num_parents=K, seed=5, mutation_prob=0.0, crossover_prob=0.5)
+    base = np.repeat(np.arange(N, dtype=float)[:, None, None], 20, axis=1).reshape(N, 5, 4)
+    pop = P.Population(base, np.arange(N, dtype=float), 7)  # elite rank r holds value r everywhere
+    kids = P.evolve_generation(pop, spec, sched, s, np.array([100.0, 0.0])).candidates[K:].reshape(N - K, 20)
+    assert kids.min() >= 0 and kids.max() <= K - 1
+    counts = np.bincount(kids[:, 0].astype(int), minlength=K)  # one parent draw per child (genes are correlated)
+    expect = kids.shape[0] / K
+    chi2 = float(((counts - expect) ** 2 / expect).sum())
+    assert chi2 < K + 6 * np.sqrt(2 * K)  # chi-square, K-1 dof
+    nd = np.array([len(np.unique(r)) for r in kids])
+    assert nd.max() <= 2
+    two = kids[nd == 2]
+    frac = (two == two.min(axis=1, keepdims=True)).mean()
+    assert abs(frac - 0.5) < 5 * np.sqrt(0.25 / two.size)
+
+
+def test_philox_breeding_matches_counter_model():
+    """The production breed stream is exactly the documented counter scheme
+    (tests/philox_model.py): parents, crossover and mutation masks bit-exact,
+    mutation noise to float rounding."""
+    from tests.philox_model import breed_draws
+
+    spec, sched = _stat_problem()
+    N, K, pm = 4000, 40, 20
+    # crossover / parents: elite rank r holds r * 1000 + gene
+    s = P.EmpcSettings(num_sims=N, num_parents=K, seed=123456789012345, mutation_prob=0.0, crossover_prob=0.37)
+    base = (np.arange(N)[:, None] * 1000.0 + np.arange(pm)[None, :]).reshape(N, 5, 4)
+    pop = P.Population(base, np.arange(N, dtype=float), 9)
+    kids = P.evolve_generation(pop, spec, sched, s, np.array([100.0, 0.0])).candidates[K:].reshape(N - K, pm)
+    parents, take, _, _ = breed_draws(s.seed, 9, N - K, pm, K, 0.37, 0.0)
+    want = np.where(take, parents[:, 1:2], parents[:, 0:1]) * 1000.0 + np.arange(pm)[None, :]
+    np.testing.assert_array_equal(kids, want)
+    # mutation: zero elites, child gene = sigma * z where mutated
+    s = P.EmpcSettings(num_sims=N, num_parents=K, seed=77, sigma_noise=np.full(4, 0.25), mutation_prob=0.3)
+    pop = P.Population(np.zeros((N, 5, 4)), np.arange(N, dtype=float), 3)
+    kids = P.evolve_generation(pop, spec, sched, s, np.array([100.0, 0.0])).candidates[K:].reshape(N - K, pm)
+    _, _, mut, z = breed_draws(77, 3, N - K, pm, K, 0.5, 0.3)
+    np.testing.assert_array_equal(kids != 0.0, mut)
+    np.testing.assert_allclose(kids[mut], 0.25 * z[mut], rtol=2e-5, atol=1e-6)
 
 
 def test_batched_instances_match_individual_solves():
