@@ -76,9 +76,9 @@ def workload(args, rank, world):
     if args.instances is not None:
         w = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=args.instances)
     if w.instances > 1:  # shard instances across ranks
-        per = (w.instances + world - 1) // world
-        first = rank * per
-        count = max(0, min(per, w.instances - first))
+        from paper_2001_04931_b200.shard import instance_range
+
+        first, count = instance_range(w.instances, rank, world)
         specs, x0s = W.build(w, first, count)
         local = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=count)
         return w, local, specs, x0s, "strong"

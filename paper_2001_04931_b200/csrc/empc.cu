@@ -95,6 +95,7 @@ class Engine final : public EngineBase {
     CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dd.device));
     variants_ = variants_for<S>(d_.NP);
     use_pdl_ = std::getenv("EMPC_NO_PDL") == nullptr;
+    if (const char* v = std::getenv("EMPC_VARIANT")) forced_ = std::atoi(v);
     phases_ = std::getenv("EMPC_PHASES") != nullptr;
     incremental_ = std::getenv("EMPC_FULL_SELECT") == nullptr;
     if (phases_) {
@@ -319,16 +320,35 @@ class Engine final : public EngineBase {
     return 1;
   }
 
+  // Default variant from measured preferences on B200 (tools/tune.py,
+  // profiles/): A in registers split over lane pairs for single problems with
+  // n <= 48, A in registers for batched small problems, smem A for n >= 64.
   const Variant<S>& pick() {
     if (forced_ >= 0) return variants_.at(forced_);
-    // heuristic default (bench.py / tests can force any variant)
-    for (auto& v : variants_) {
-      if (v.dq != dense_) continue;
-      if (dense_) return v;
-      if (v.areg && v.RR == 1) return v;  // A in registers, one row per thread: most threads per candidate
+    auto find = [&](int RR, int CC, bool areg, int ks) -> const Variant<S>* {
+      for (auto& v : variants_)
+        if (v.RR == RR && v.CC == CC && v.areg == areg && v.ks == ks && v.dq == dense_) return &v;
+      return nullptr;
+    };
+    if (!dense_ && sizeof(S) == 4) {
+      const Variant<S>* pref[4] = {nullptr, nullptr, nullptr, nullptr};
+      if (d_.NP <= 48 && I_ == 1) {
+        pref[0] = find(2, 4, true, 2);
+        pref[1] = find(1, 4, true, 1);
+      } else if (d_.NP <= 48) {
+        pref[0] = find(2, 4, true, 1);
+        pref[1] = find(1, 4, true, 1);
+      } else {
+        pref[0] = find(2, 4, false, 1);
+        pref[1] = find(4, 4, false, 1);
+      }
+      for (auto* v : pref)
+        if (v) return *v;
     }
     for (auto& v : variants_)
-      if (v.dq == dense_ && !v.areg && v.CC == 4) return v;
+      if (v.dq == dense_ && (dense_ || v.areg)) return v;
+    for (auto& v : variants_)
+      if (v.dq == dense_) return v;
     return variants_.front();
   }
 

@@ -1,0 +1,70 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports every
+symbol include/empc_b200.h declares.  CPU only (no compute calls)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2001_04931_b200 import _native as nat
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "empc_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(empc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    assert declared_functions() == sorted(nat.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(nat.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a():
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built")
+    out = subprocess.run(["cuobjdump", "--list-elf", nat.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_rollout_kernels_use_fp32_fma():
+    """The rollout hot loop is FFMA work (SURVEY §8d roofline): its SASS is
+    dominated by FFMA and carries no legacy HMMA tensor path."""
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built")
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun",
+                           "_ZN4empc14rollout_kernelIfLi48ELi1ELi4ELb1ELb0ELi1ELi384EEEvNS_11RolloutArgsIT_EE",
+                           nat.LIB_PATH], capture_output=True, text=True).stdout
+    assert sass.count("FFMA") >= 192  # 48 columns x 4 candidates, fully unrolled
+    assert "HMMA" not in sass
+
+
+def test_load_without_gpu_does_not_touch_the_device():
+    lib = nat.load()
+    assert lib.empc_last_error(None) is not None
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(RuntimeError, match="missing"):
+        _load_missing(tmp_path)
+
+
+def _load_missing(tmp_path):
+    saved = nat._lib
+    nat._lib = None
+    try:
+        nat.load(str(tmp_path / "nope.so"))
+    finally:
+        nat._lib = saved
