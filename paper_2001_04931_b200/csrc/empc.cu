@@ -371,7 +371,7 @@ class Engine final : public EngineBase {
                                                                               : nullptr;
     a.qlist = (char*)qlist_ + (size_t)(evolve & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
     a.qcap = qcap_;
-    if (phases_ && (size_t)L.tiles * I_ * 8 <= dbg_n_) {
+    if (phases_ && (size_t)L.tiles * I_ * 16 <= dbg_n_) {
       a.dbg = dbg_;
       dbg_ctas_ = (int)(L.tiles * I_);
     }
@@ -679,22 +679,18 @@ class Engine final : public EngineBase {
       *rollout_ms = (float)(sum / ((double)reps2 * std::max(nr, 1)));
     }
     if (phases_ && dbg_ctas_ > 0) {
-      // phase durations of the last rollout launch: mean and max over CTAs, relative to the earliest start
-      std::vector<unsigned long long> t((size_t)dbg_ctas_ * 8);
+      // phase marks of the last rollout launch: mean over CTAs, relative to each CTA's start
+      std::vector<unsigned long long> t((size_t)dbg_ctas_ * 16);
       CK(cudaMemcpy(t.data(), dbg_, t.size() * 8, cudaMemcpyDeviceToHost));
-      unsigned long long t0 = ~0ull;
-      for (int c = 0; c < dbg_ctas_; ++c) t0 = std::min(t0, t[(size_t)c * 8]);
-      double mean[7] = {0}, mx[7] = {0};
-      for (int c = 0; c < dbg_ctas_; ++c)
-        for (int i = 0; i < 7; ++i) {
-          const double v = (double)(t[(size_t)c * 8 + i] - t0) * 1e-3;
-          mean[i] += v / dbg_ctas_;
-          mx[i] = std::max(mx[i], v);
-        }
-      std::fprintf(stderr, "phases(us from first CTA start) start/p0/wait/genes/bu/loop/end mean:");
-      for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %.2f", mean[i]);
-      std::fprintf(stderr, " | max:");
-      for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %.2f", mx[i]);
+      const int order[13] = {0, 7, 8, 1, 2, 9, 10, 3, 11, 12, 4, 5, 6};
+      const char* names[13] = {"start", "p0", "sync", "rng", "wait", "elite", "src", "genes", "bu", "cost", "x0", "loop", "end"};
+      std::fprintf(stderr, "phases(us since CTA start, mean over %d CTAs):", dbg_ctas_);
+      for (int q = 0; q < 13; ++q) {
+        double mean = 0;
+        for (int c = 0; c < dbg_ctas_; ++c)
+          mean += (double)(t[(size_t)c * 16 + order[q]] - t[(size_t)c * 16]) * 1e-3 / dbg_ctas_;
+        std::fprintf(stderr, " %s=%.2f", names[q], mean);
+      }
       std::fprintf(stderr, "\n");
     }
   }

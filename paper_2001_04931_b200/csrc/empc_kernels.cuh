@@ -81,7 +81,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define EMPC_MARK(I)                                                                                  \
   if (a.dbg != nullptr && threadIdx.x == 0)                                                          \
-    a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (I)] = gtimer();
+    a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (I)] = gtimer();
 
 template <typename S>
 struct Geo {
@@ -140,7 +140,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // (1) wait for the producer, elite carry-over and breeding; (2) B at the
 // knots and the knot-space input cost; (3) the horizon recursion.
 
-template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, int MAXT>
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a) {
   constexpr int NRG = NP / RR;
   constexpr int VEC = Geo<S>::VEC;
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   constexpr int NSPLIT = (RR * CC >= 8) ? 1 : ((RR * CC >= 4) ? 2 : 4);
   constexpr int NJ = NP / VEC / KS;  // 16-byte column groups per reduction half
   constexpr int NPH = NP / KS;       // columns per reduction half
+  static_assert(!WS || 32 % (NRG * KS) == 0, "warp-synchronous variants need whole candidate groups per warp");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Dims& d = a.d;
   const StageLayout& SL = a.SL;
@@ -197,11 +198,13 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       sC[k] = a.cw[k];
     }
     for (int e = tid; e < p * p; e += nthr) sG[e] = a.G[e];
+#pragma unroll 8
     for (int e = tid; e < NP * NP; e += nthr) {
       const int i = e / NP, j = e - (e / NP) * NP;
       As[i * NPS + j] = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
       if constexpr (DQ) Qs[i * NPS + j] = (i < n && j < n) ? (S)P[SL.q + i * n + j] : S(0);
     }
+#pragma unroll 8
     for (int e = tid; e < NP * m; e += nthr) {
       const int i = e / m, l = e - (e / m) * m;
       Bs[i * (m + 1) + l] = i < n ? (S)P[SL.bd + i * m + l] : S(0);
@@ -239,7 +242,9 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
     }
   }
 
+  EMPC_MARK(7)
   __syncthreads();  // phase-0 smem (bounds, sigma) is read by every thread below
+  EMPC_MARK(8)
   // ---- phase 1a: random draws -- counter-based, so also independent of the
   // producer grid (the run parameters are staged by the host copy)
   const RunParams rp = *a.run;
@@ -307,6 +312,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
     }
   }
   if (cnt <= 0) return;
+  EMPC_MARK(9)
   if (breed) {
     for (int c = tid; c < cnt; c += nthr) {  // elite ranks -> population rows
       src[2 * c] = a.elite_idx[(size_t)inst * d.K + src[2 * c]];
@@ -314,7 +320,28 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
     }
   }
   __syncthreads();  // src, phase-0/1a smem
+  EMPC_MARK(10)
   // candidate knots -> UsT[gene][cand] (+ the population rows)
+  if (philox_breed) {
+    // crossover, mutation, clip (K/empc.py:201-204): a tight loop so the
+    // parent gathers of several genes are in flight together
+#pragma unroll 8
+    for (int e = tid; e < cnt * pm; e += nthr) {
+      const int c = e / pm, g = e - (e / pm) * pm;
+      const int l = g % m;
+      const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
+      const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+      const S lo = cumin[l], hi = cumax[l];
+      S v = par + UsT[g * tPS + c];
+      v = v < lo ? lo : (v > hi ? hi : v);
+      a.pop_out[(pop_base + a.row0 + tile0 + c) * pm + g] = v;
+      UsT[g * tPS + c] = v;
+    }
+    for (int e = cnt * pm + tid; e < tileP * pm; e += nthr) {
+      const int c = e / pm, g = e - (e / pm) * pm;
+      UsT[g * tPS + c] = S(0);
+    }
+  } else
 #pragma unroll 4
   for (int e = tid; e < tileP * pm; e += nthr) {
     const int c = e / pm, g = e - (e / pm) * pm;
@@ -393,49 +420,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       for (int r = 0; r < RR; ++r) sts_vec<S, CC>(BUT + (j * NP + rg + r * NRG) * tPS + c0, acc[r]);
     }
   }
-  // input cost as the knot quadratic z'(W'W (x) R)z, z = U - u_goal
-  // (K/empc.py:100-101): one warp per candidate, lanes over channels
-  for (int c = warp; c < cnt; c += nwarps) {
-    S val = S(0);
-    for (int l = lane; l < m; l += 32) {
-      const S ugl = cug[l];
-      S gz[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) gz[q] = S(0);
-      if (p <= 8) {
-        for (int b = 0; b < p; ++b) {
-          S rz;
-          if (a.r_diag) {
-            rz = crd[l] * (UsT[(b * m + l) * tPS + c] - ugl);
-          } else {
-            rz = S(0);
-            for (int l2 = 0; l2 < m; ++l2)
-              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (q < p) gz[q] = fma(sG[q * p + b], rz, gz[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < p) val = fma(UsT[(q * m + l) * tPS + c] - ugl, gz[q], val);
-      } else {
-        for (int q = 0; q < p; ++q) {
-          S gzq = S(0);
-          for (int b = 0; b < p; ++b) {
-            S rz = S(0);
-            for (int l2 = 0; l2 < m; ++l2)
-              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
-            gzq = fma(sG[q * p + b], rz, gzq);
-          }
-          val = fma(UsT[(q * m + l) * tPS + c] - ugl, gzq, val);
-        }
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, off);
-    if (lane == 0) cU[c] = val;
-  }
+  EMPC_MARK(11)
   // model rows: A (Delta = Ad - I) from smem into registers
   S areg[AREG ? RR : 1][AREG ? NPH : 1];
   if constexpr (AREG) {
@@ -449,6 +434,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
         for (int q = 0; q < VEC; ++q) areg[r][jv * VEC + q] = t[q];
       }
   }
+  EMPC_MARK(12)
   S qv[RR], xgv[RR], qxg[RR], xo[RR][CH];
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
@@ -466,9 +452,56 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
 #pragma unroll
     for (int q = 0; q < CH; ++q) xo[r][q] = cx0[row];
   }
+  // input cost as the knot quadratic z'(W'W (x) R)z, z = U - u_goal
+  // (K/empc.py:100-101): each thread seeds the state-cost accumulators of its
+  // candidates with the channels l = rg (mod NRG); the row-group reduction at
+  // the end then sums both terms.
   S cst[CH];
 #pragma unroll
   for (int q = 0; q < CH; ++q) cst[q] = S(0);
+  if (active) {
+    for (int l = rg; l < m; l += NRG) {
+      const S ugl = cug[l];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int c = ce + q;
+        S val = S(0);
+        if (p <= 8) {
+          S gz[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) gz[t] = S(0);
+          for (int b = 0; b < p; ++b) {
+            S rz;
+            if (a.r_diag) {
+              rz = crd[l] * (UsT[(b * m + l) * tPS + c] - ugl);
+            } else {
+              rz = S(0);
+              for (int l2 = 0; l2 < m; ++l2)
+                rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (t < p) gz[t] = fma(sG[t * p + b], rz, gz[t]);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < p) val = fma(UsT[(t * m + l) * tPS + c] - ugl, gz[t], val);
+        } else {
+          for (int t = 0; t < p; ++t) {
+            S gzt = S(0);
+            for (int b = 0; b < p; ++b) {
+              S rz = S(0);
+              for (int l2 = 0; l2 < m; ++l2)
+                rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
+              gzt = fma(sG[t * p + b], rz, gzt);
+            }
+            val = fma(UsT[(t * m + l) * tPS + c] - ugl, gzt, val);
+          }
+        }
+        cst[q] += val;
+      }
+    }
+  }
   __syncthreads();  // Bs (in XC) consumed; BUT / cU visible
   // x_0 = x0 for every candidate (K/empc.py:109)
   for (int e = tid; e < tileP * NPS; e += nthr) {
@@ -569,8 +602,12 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
         if (active) xw[(ce + q) * NPS + row] = xn;
       }
     }
-    __syncthreads();
+    // WS: all rows of a candidate group live in one warp, so the state
+    // exchange of a step only needs a warp-level barrier and warps run
+    // their horizons independently
+    if constexpr (WS) __syncwarp(); else __syncthreads();
   }
+  if constexpr (WS) __syncthreads();
   if constexpr (DQ) {
     // terminal state term e_T' Q e_T
     const S* xb = XC + (T & 1) * tileP * NPS + c0 * NPS;
@@ -599,7 +636,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   for (int c = tid; c < cnt; c += nthr) {
     S s = S(0);
     for (int g = 0; g < NRG; ++g) s += red[g * tPS + c];
-    const S cost = c0s + cU[c] + s;
+    const S cost = c0s + s;
     const int row = a.row0 + tile0 + c;
     a.cost_out[pop_base + row] = cost;
     if (qual) {

@@ -13,6 +13,7 @@ struct Variant {
   int NP, RR, CC;
   bool areg, dq;
   int ks;
+  bool ws;
   int maxt;
   void (*kernel)(const RolloutArgs<S>);
   const char* name;
@@ -26,10 +27,11 @@ constexpr int maxt_for(int NP, int RR, int CC, bool areg, int elem, int KS) {
   return regs <= 64 ? 1024 : regs <= 85 ? 768 : regs <= 128 ? 512 : regs <= 168 ? 384 : 256;
 }
 
-#define RVK(S, NP, RR, CC, AR, DQ, KS)                                                                     \
-  Variant<S>{NP, RR, CC, AR, DQ, KS, maxt_for(NP, RR, CC, AR, sizeof(S), KS),                             \
-             &rollout_kernel<S, NP, RR, CC, AR, DQ, KS, maxt_for(NP, RR, CC, AR, sizeof(S), KS)>,          \
-             #S " NP" #NP " RR" #RR " CC" #CC " areg=" #AR " dq=" #DQ " ks=" #KS}
+#define RVW(S, NP, RR, CC, AR, DQ, KS, WS)                                                                 \
+  Variant<S>{NP, RR, CC, AR, DQ, KS, WS, maxt_for(NP, RR, CC, AR, sizeof(S), KS),                         \
+             &rollout_kernel<S, NP, RR, CC, AR, DQ, KS, WS, maxt_for(NP, RR, CC, AR, sizeof(S), KS)>,      \
+             #S " NP" #NP " RR" #RR " CC" #CC " areg=" #AR " dq=" #DQ " ks=" #KS " ws=" #WS}
+#define RVK(S, NP, RR, CC, AR, DQ, KS) RVW(S, NP, RR, CC, AR, DQ, KS, false)
 #define RV(S, NP, RR, CC, AR, DQ) RVK(S, NP, RR, CC, AR, DQ, 1)
 
 
