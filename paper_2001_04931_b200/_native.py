@@ -67,11 +67,13 @@ class empc_run_args(C.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load the CUDA library (once).  Raises if it is missing: no fallback."""
+def load(path: str | None = None):
+    """Load the CUDA library (once).  Raises if it is missing: no fallback.
+    ``EMPC_LIB`` overrides the path (experiment builds)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("EMPC_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise RuntimeError(
             f"{path} is missing: build the CUDA extension first "

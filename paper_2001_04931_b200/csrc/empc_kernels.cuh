@@ -209,12 +209,15 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       const int i = e / m, l = e - (e / m) * m;
       Bs[i * (m + 1) + l] = i < n ? (S)P[SL.bd + i * m + l] : S(0);
     }
+    // the recursion runs in error coordinates e = x - x_goal:
+    //   e_{k+1} = e_k + Delta e_k + (drive_k + Delta x_goal)
+    // so w picks up Delta x_goal (rows of W sum to one) and e_0 = x0 - x_goal
     for (int i = tid; i < NP; i += nthr) {
       const bool ok = i < n;
-      cw_[i] = ok ? (S)P[SL.wd + i] : S(0);
+      cw_[i] = ok ? (S)P[SL.wd + i] : S(0);  // + Delta x_goal below, from As
       cqd[i] = ok ? (S)P[SL.q + i * n + i] : S(0);
       cxg[i] = ok ? (S)P[SL.xg + i] : S(0);
-      cx0[i] = ok ? (S)X[SL.x0 + i] : S(0);
+      cx0[i] = ok ? (S)(X[SL.x0 + i] - P[SL.xg + i]) : S(0);
     }
     for (int l = tid; l < m; l += nthr) {
       cug[l] = (S)P[SL.ug + l];
@@ -244,6 +247,14 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
 
   EMPC_MARK(7)
   __syncthreads();  // phase-0 smem (bounds, sigma) is read by every thread below
+  // w += Delta x_goal (error coordinates): one warp per row group, lanes over columns
+  for (int i = warp; i < n; i += nwarps) {
+    S acc = S(0);
+    for (int j = lane; j < n; j += 32) acc = fma(As[i * NPS + j], cxg[j], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
+    if (lane == 0) cw_[i] += acc;
+  }
   EMPC_MARK(8)
   // ---- phase 1a: random draws -- counter-based, so also independent of the
   // producer grid (the run parameters are staged by the host copy)
@@ -435,20 +446,11 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       }
   }
   EMPC_MARK(12)
-  S qv[RR], xgv[RR], qxg[RR], xo[RR][CH];
+  S qv[RR], xo[RR][CH];  // state rows in error coordinates
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
     const int row = rg + r * NRG;
     qv[r] = DQ ? S(0) : cqd[row];
-    xgv[r] = cxg[row];
-    qxg[r] = S(0);
-    if constexpr (DQ) {
-      if (row < n) {
-        double s = 0.0;
-        for (int j = 0; j < n; ++j) s = fma(P[SL.q + row * n + j], P[SL.xg + j], s);
-        qxg[r] = (S)s;
-      }
-    }
 #pragma unroll
     for (int q = 0; q < CH; ++q) xo[r][q] = cx0[row];
   }
@@ -515,20 +517,24 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
 
   // partial products of the rows with this thread's column half, with
   // software-pipelined 16-byte loads (the next column group is in flight
-  // while the current one is consumed); KS == 2 folds the halves with one
-  // shuffle.  A macro, not a lambda, so the register arrays stay in registers.
-#define EMPC_MATVEC(FROMREG, MS, XB, OUT)                                                             \
+  // while the current one is consumed).  With KS == 2 each lane lists its
+  // own CH candidates first (base XO) and its partner's second (base XP), so
+  // folding the halves is one shuffle + one add per result, no selects.
+  // A macro, not a lambda, so the register arrays stay in registers.
+#define EMPC_MATVEC(FROMREG, MS, XO, XP, OUT)                                                         \
   {                                                                                                   \
     S part_[RR][CC][NSPLIT];                                                                          \
     _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
     _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                    \
     _Pragma("unroll") for (int s = 0; s < NSPLIT; ++s) part_[r][q][s] = S(0);                         \
     S xv_[2][CC][VEC];                                                                                \
-    _Pragma("unroll") for (int q = 0; q < CC; ++q) lds_vec<S, VEC>((XB) + q * NPS + jbase, xv_[0][q]); \
+    _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                    \
+      lds_vec<S, VEC>((q < CH ? (XO) + q * NPS : (XP) + (q - CH) * NPS), xv_[0][q]);                 \
     _Pragma("unroll") for (int jj = 0; jj < NJ; ++jj) {                                               \
       if (jj + 1 < NJ) {                                                                              \
         _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                \
-          lds_vec<S, VEC>((XB) + q * NPS + jbase + (jj + 1) * VEC, xv_[(jj + 1) & 1][q]);             \
+          lds_vec<S, VEC>((q < CH ? (XO) + q * NPS : (XP) + (q - CH) * NPS) + (jj + 1) * VEC,        \
+                          xv_[(jj + 1) & 1][q]);                                                      \
       }                                                                                               \
       S av_[RR][VEC];                                                                                 \
       _Pragma("unroll") for (int r = 0; r < RR; ++r) {                                                \
@@ -543,80 +549,84 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                  \
         part_[r][q][t % NSPLIT] = fma(av_[r][t], xv_[jj & 1][q][t], part_[r][q][t % NSPLIT]);         \
     }                                                                                                 \
-    S sum_[RR][CC];                                                                                   \
-    _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
-    _Pragma("unroll") for (int q = 0; q < CC; ++q) {                                                  \
-      sum_[r][q] = part_[r][q][0];                                                                    \
-      _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) sum_[r][q] += part_[r][q][s];                \
-    }                                                                                                 \
     _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
     _Pragma("unroll") for (int q = 0; q < CH; ++q) {                                                  \
+      S mine_ = part_[r][q][0];                                                                       \
+      _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) mine_ += part_[r][q][s];                     \
       if constexpr (KS == 2) {                                                                        \
-        /* keep my half, send the partner its half: one shuffle per result */                        \
-        const S mine_ = ks ? sum_[r][CH + q] : sum_[r][q];                                            \
-        const S give_ = ks ? sum_[r][q] : sum_[r][CH + q];                                            \
-        (OUT)[r][q] = mine_ + __shfl_xor_sync(0xFFFFFFFFu, give_, 16);                                \
-      } else {                                                                                        \
-        (OUT)[r][q] = sum_[r][q];                                                                     \
+        S give_ = part_[r][CH + q][0];                                                                \
+        _Pragma("unroll") for (int s = 1; s < NSPLIT; ++s) give_ += part_[r][CH + q][s];              \
+        mine_ += __shfl_xor_sync(0xFFFFFFFFu, give_, 16);                                             \
       }                                                                                               \
+      (OUT)[r][q] = mine_;                                                                            \
     }                                                                                                 \
   }
 
-  // ---- phase 3: horizon recursion x_{k+1} = x_k + Delta x_k + drive_k
-  // (K/empc.py:110-112), state cost fused per step (K/empc.py:113-118).
-  // The knot pair of the drive changes p - 1 times over the horizon: the
-  // interpolation endpoints B U_j + w are cached in registers.
+  // ---- phase 3: horizon recursion in error coordinates,
+  // e_{k+1} = e_k + Delta e_k + drive'_k (K/empc.py:110-112), state cost
+  // fused per step (K/empc.py:113-118).  The knot pair of the drive changes
+  // p - 1 times over the horizon: the endpoint b1 and slope b2 - b1 of the
+  // interpolation are cached in registers.
+  // loop-invariant addresses: own / partner candidate rows of both buffers
+  const S* xo0 = XC + (size_t)ce * NPS + jbase;
+  const S* xp0 = XC + (size_t)(c0 + (ks ^ 1) * CH) * NPS + jbase;
+  const size_t bufstride = (size_t)tileP * NPS;
+  S* xw0 = XC + (size_t)ce * NPS + rg;
   int ci1 = -1, ci2 = -1;
-  S b1[RR][CH], b2[RR][CH];
+  S b1[RR][CH], db[RR][CH];
+  const int* __restrict__ si1 = sI1;
+  const int* __restrict__ si2 = sI2;
   for (int k = 0; k < T; ++k) {
-    const S* xb = XC + (k & 1) * tileP * NPS + c0 * NPS;
-    S* xw = XC + ((k & 1) ^ 1) * tileP * NPS;
+    const size_t rd = (k & 1) ? bufstride : 0, wr = (k & 1) ? 0 : bufstride;
     S ax[RR][CH];
-    EMPC_MATVEC(AREG, As, xb, ax)
+    EMPC_MATVEC(AREG, As, xo0 + rd, xp0 + rd, ax)
     S qx[DQ ? RR : 1][DQ ? CH : 1];
-    if constexpr (DQ) EMPC_MATVEC(false, Qs, xb, qx)
-    const int i1 = sI1[k], i2 = sI2[k];
-    const S ck = sC[k], c1 = S(1) - ck;
+    if constexpr (DQ) EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qx)
+    const int i1 = si1[k], i2 = si2[k];
+    const S ck = sC[k];
     if (i1 != ci1 || i2 != ci2) {  // uniform across the CTA
       ci1 = i1;
       ci2 = i2;
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
+        S t2[CH];
         lds_vec<S, CH>(BUT + (i1 * NP + rg + r * NRG) * tPS + ce, b1[r]);
-        lds_vec<S, CH>(BUT + (i2 * NP + rg + r * NRG) * tPS + ce, b2[r]);
+        lds_vec<S, CH>(BUT + (i2 * NP + rg + r * NRG) * tPS + ce, t2);
+#pragma unroll
+        for (int q = 0; q < CH; ++q) db[r][q] = t2[q] - b1[r][q];
       }
     }
+    S* xw = xw0 + wr;
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
-      const int row = rg + r * NRG;
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
-        if constexpr (DQ) cst[q] = fma(xo[r][q] - xgv[r], qx[r][q] - qxg[r], cst[q]);  // cost of x_k
-        const S drive = fma(ck, b2[r][q], c1 * b1[r][q]);
-        const S xn = xo[r][q] + (ax[r][q] + drive);
-        xo[r][q] = xn;
-        if constexpr (!DQ) {
-          const S e = xn - xgv[r];
-          cst[q] = fma(qv[r] * e, e, cst[q]);  // cost of x_{k+1}, diagonal Q
-        }
-        if (active) xw[(ce + q) * NPS + row] = xn;
+        if constexpr (DQ) cst[q] = fma(xo[r][q], qx[r][q], cst[q]);  // e_k' Q e_k
+        const S en = xo[r][q] + fma(ck, db[r][q], ax[r][q] + b1[r][q]);
+        xo[r][q] = en;
+        if constexpr (!DQ) cst[q] = fma(qv[r] * en, en, cst[q]);  // e_{k+1}' diag(Q) e_{k+1}
+#ifndef EMPC_EXP_NOSTS
+        if (active) xw[q * NPS + r * NRG] = en;
+#endif
       }
     }
     // WS: all rows of a candidate group live in one warp, so the state
     // exchange of a step only needs a warp-level barrier and warps run
     // their horizons independently
+#ifndef EMPC_EXP_NOBAR
     if constexpr (WS) __syncwarp(); else __syncthreads();
+#endif
   }
   if constexpr (WS) __syncthreads();
   if constexpr (DQ) {
     // terminal state term e_T' Q e_T
-    const S* xb = XC + (T & 1) * tileP * NPS + c0 * NPS;
+    const size_t rd = (T & 1) ? bufstride : 0;
     S qf[RR][CH];
-    EMPC_MATVEC(false, Qs, xb, qf)
+    EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qf)
 #pragma unroll
     for (int r = 0; r < RR; ++r)
 #pragma unroll
-      for (int q = 0; q < CH; ++q) cst[q] = fma(xo[r][q] - xgv[r], qf[r][q] - qxg[r], cst[q]);
+      for (int q = 0; q < CH; ++q) cst[q] = fma(xo[r][q], qf[r][q], cst[q]);
   }
   EMPC_MARK(5)
   // ---- deterministic reduction over row groups (BUT is free now)
