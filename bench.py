@@ -182,6 +182,63 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_population_sharded(args, rank, world):
+    """C4 over W GPUs: one population split over ranks, one NCCL all-gather of
+    the ranks' top-K entries per generation.  Strong scaling:
+    the total population is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_04931_b200 import workloads as W
+    from paper_2001_04931_b200.shard import PopulationShard, solve_population_sharded
+
+    w = W.WORKLOADS[args.config]
+    specs, x0s = W.build(w)
+    shard = PopulationShard(specs[0], w.schedule(), w.settings(), rank, world)
+    K, eb = shard.K, shard.entry_bytes
+    gathered = torch.empty(world * K * eb, dtype=torch.uint8, device="cuda")
+
+    def all_gather(local):
+        dist.all_gather_into_tensor(gathered, local)
+        return gathered
+
+    for _ in range(max(args.warmup, 3)):
+        solve_population_sharded(shard, x0s[0], all_gather)
+    sampler = ClockSampler(0)
+    times = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u, best, cost = solve_population_sharded(shard, x0s[0], all_gather)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    dist.barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([sum(times)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    units = w.cand_steps_per_solve * args.steps
+    value = units / (total_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (reference recipe: linearized N-link arms, SURVEY §8d)",
+        "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]} (population sharded over {world} GPUs, "
+                               "per-generation NCCL all-gather of the ranks' top-K)", "dof": w.dof, "T": w.T,
+                   "p": w.p, "N": w.N, "K": w.K, "G": w.G, "instances": 1, "l2": "not flushed (NCCL path)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(sum(v.nbytes for v in x0s) + 8 * 9 * 96 * 96),
+                "d2h_bytes_per_step": int(u.nbytes + best.nbytes + 8), "api": "shard.solve_population_sharded"},
+        "clocks": clocks,
+        "gpu_launches": (2 * w.G + 1) * args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
@@ -198,6 +255,8 @@ def run_ours(args):
     from paper_2001_04931_b200 import _native as nat
     from paper_2001_04931_b200 import empc as E
 
+    if world > 1 and args.config == "c4":
+        return run_population_sharded(args, rank, world)
     w_total, w, specs, x0s, scaling = workload(args, rank, world)
     sched = w.schedule()
     st = w.settings()

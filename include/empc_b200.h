@@ -148,6 +148,28 @@ int empc_set_variant(empc_handle* h, int32_t variant);
 /* Rollout CTAs per SM for the launch plan (0 restores the heuristic). */
 int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm);
 
+/* Population sharding over GPUs (K/empc.py:174-208 split
+ * across ranks).  A rank holds the K elites (replicated) and the children of
+ * global child indices [child_base, child_base + n_children) -- and, for the
+ * cold start, the initial candidates [init_base, init_base + n_init).  The
+ * handle's num_sims must be >= K + max(n_children, n_init).  Per generation:
+ * empc_shard_export writes this rank's top-K candidates as K self-contained
+ * entries of empc_shard_entry_bytes bytes into a DEVICE buffer; the caller
+ * all-gathers the W buffers (NCCL over NVLink); empc_shard_import ranks the
+ * W*K entries and installs the global top-K as elites (reporting the global
+ * best); empc_shard_evolve breeds and scores this rank's children.  Keys use
+ * global rows and the RNG counters global child indices, so the result is
+ * identical to the unsharded solve for any world size. */
+int empc_shard_setup(empc_handle* h, int64_t child_base, int32_t n_children, int64_t init_base, int32_t n_init,
+                     int32_t owns_elites);
+int empc_shard_entry_bytes(empc_handle* h, int64_t* bytes);
+int empc_shard_init(empc_handle* h, const empc_run_args* args);
+int empc_shard_export(empc_handle* h, void* dev_entries);
+int empc_shard_import(empc_handle* h, const void* dev_all, int32_t world, double* u_out, double* best_out,
+                      double* best_cost, int64_t* best_row);
+int empc_shard_evolve(empc_handle* h, const empc_run_args* args);
+int empc_shard_read(empc_handle* h, double* cands, double* costs);
+
 /* Known-answer seam for the in-kernel counter-based RNG: Philox4x32-10 of
  * `count` (ctr[4], key[2]) pairs evaluated on the device. */
 int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out);

@@ -24,7 +24,8 @@ EXPORTS = (
     "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_problems",
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
-    "empc_set_variant", "empc_set_occupancy", "empc_philox",
+    "empc_set_variant", "empc_set_occupancy", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
+    "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read",
 )
 
 
@@ -101,6 +102,13 @@ def load(path: str | None = None):
         "empc_set_variant": (C.c_int, [P, I32]),
         "empc_set_occupancy": (C.c_int, [P, I32]),
         "empc_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), I32, C.POINTER(C.c_uint32)]),
+        "empc_shard_setup": (C.c_int, [P, I64, I32, I64, I32, I32]),
+        "empc_shard_entry_bytes": (C.c_int, [P, C.POINTER(I64)]),
+        "empc_shard_init": (C.c_int, [P, C.POINTER(empc_run_args)]),
+        "empc_shard_export": (C.c_int, [P, P]),
+        "empc_shard_import": (C.c_int, [P, P, I32, D, D, D, C.POINTER(I64)]),
+        "empc_shard_evolve": (C.c_int, [P, C.POINTER(empc_run_args)]),
+        "empc_shard_read": (C.c_int, [P, D, D]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -79,6 +79,13 @@ class EngineBase {
   virtual int num_variants() = 0;
   virtual void set_variant(int) = 0;
   virtual void set_occupancy(int) = 0;
+  virtual void shard_setup(long long, int, long long, int, int) = 0;
+  virtual size_t shard_entry_size() = 0;
+  virtual void shard_init(const empc_run_args&) = 0;
+  virtual void shard_export(void*) = 0;
+  virtual void shard_import(const void*, int, double*, double*, double*, long long*) = 0;
+  virtual void shard_evolve(const empc_run_args&) = 0;
+  virtual void shard_read(double*, double*) = 0;
 };
 
 template <typename S>
@@ -361,6 +368,7 @@ class Engine final : public EngineBase {
     a.d = d_; a.SL = SL_; a.mode = mode; a.r_diag = r_diag_ ? 1 : 0;
     a.nc = nc; a.row0 = row0; a.rows = rows;
     a.tile = L.tile; a.tileP = L.tileP; a.tPS = tps_for(L.tileP); a.evolve = evolve;
+    a.cand_base = cand_base_;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
     a.pop_in = pin; a.cost_in = cin; a.pop_out = pout; a.cost_out = cout;
@@ -695,6 +703,107 @@ class Engine final : public EngineBase {
     }
   }
 
+  // -- population sharding: see shard_export_kernel ------------------
+  void shard_setup(long long child_base, int n_children, long long init_base, int n_init, int owns_elites) override {
+    if (I_ != 1) throw InvalidArg{"population sharding needs a single-instance handle"};
+    if (n_children < 0 || n_init < 0 || d_.K + std::max(n_children, n_init) > d_.N)
+      throw InvalidArg{"shard does not fit the handle (num_sims must be >= K + max(children, init) rows)"};
+    sh_child_base_ = child_base;
+    sh_children_ = n_children;
+    sh_init_base_ = init_base;
+    sh_init_ = n_init;
+    sh_owns_elites_ = owns_elites;
+    sh_on_ = true;
+  }
+  size_t shard_entry_size() override { return shard_entry_bytes<S>(d_.pm); }
+  void shard_check() {
+    if (!sh_on_) throw InvalidArg{"empc_shard_setup first"};
+  }
+  void shard_init(const empc_run_args& r) override {
+    shard_check();
+    empc_run_args rr = r;
+    rr.init = 1;
+    rr.slot_in = -1;
+    stage_run(rr);
+    pdl_next_ = false;
+    cand_base_ = (int)sh_init_base_;
+    launch_rollout(kInitPhilox, sh_init_, d_.K, d_.N, 0, nullptr, nullptr, pop_[0], cost_[0]);
+    cand_base_ = 0;
+    pdl_next_ = false;
+    sh_cur_ = 0;
+    sh_init_phase_ = true;
+    CK(cudaStreamSynchronize(stream_));
+  }
+  int rank_grid(int M) const { return std::max(1, std::min(sms_, (M + 15) / 16)); }
+  void shard_export(void* dev_out) override {
+    shard_check();
+    const int incl = (sh_owns_elites_ && !sh_init_phase_) ? 1 : 0;
+    const int nl = sh_init_phase_ ? sh_init_ : sh_children_;
+    const long long gbase = sh_init_phase_ ? sh_init_base_ : (long long)d_.K + sh_child_base_;
+    const int M = (incl ? d_.K : 0) + nl;
+    const size_t smem = (size_t)M * (sizeof(typename OrdOf<S>::T) + 2 * sizeof(int));
+    if (smem > (size_t)kMaxSmem - 1024) throw InvalidArg{"shard too large for the export kernel"};
+    CK(cudaFuncSetAttribute(shard_export_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+    shard_export_kernel<S><<<rank_grid(M), 256, smem, stream_>>>(pop_[sh_cur_], cost_[sh_cur_], d_.K, d_.pm, incl, nl,
+                                                                  gbase, (unsigned char*)dev_out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream_));
+  }
+  void shard_import(const void* dev_all, int world, double* u, double* best, double* cost, long long* grow) override {
+    shard_check();
+    const int M = world * d_.K;
+    const size_t smem = (size_t)M * (sizeof(unsigned long long) + sizeof(unsigned));
+    if (smem > (size_t)kMaxSmem - 1024) throw InvalidArg{"world * num_parents too large for the import kernel"};
+    CK(cudaFuncSetAttribute(shard_import_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+    shard_import_kernel<S><<<rank_grid(M), 256, smem, stream_>>>((const unsigned char*)dev_all, M, d_.K, d_.pm, d_.m,
+                                                                  pop_[sh_cur_], cost_[sh_cur_], elite_, out_d_);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * out_stride_, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    sh_init_phase_ = false;
+    if (u) std::memcpy(u, out_h_, sizeof(double) * d_.m);
+    if (best) std::memcpy(best, out_h_ + d_.m, sizeof(double) * d_.pm);
+    if (cost) *cost = out_h_[d_.m + d_.pm];
+    if (grow) *grow = (long long)out_h_[d_.m + d_.pm + 1];
+  }
+  void shard_evolve(const empc_run_args& r) override {
+    shard_check();
+    if (sh_init_phase_) throw InvalidArg{"import the elites before evolving"};
+    empc_run_args rr = r;
+    rr.init = 1;  // staging only: the population stays where it is
+    stage_run(rr);
+    pdl_next_ = false;
+    cand_base_ = (int)sh_child_base_;
+    int* saved_q = qcount_;
+    qcount_ = nullptr;
+    const bool saved_inc = incremental_;
+    incremental_ = false;
+    launch_rollout(kBreedPhilox, sh_children_, d_.K, d_.N, 0, pop_[sh_cur_], cost_[sh_cur_], pop_[sh_cur_ ^ 1],
+                   cost_[sh_cur_ ^ 1]);
+    incremental_ = saved_inc;
+    qcount_ = saved_q;
+    cand_base_ = 0;
+    pdl_next_ = false;
+    sh_cur_ ^= 1;
+    CK(cudaStreamSynchronize(stream_));
+  }
+  void shard_read(double* cands, double* costs) override {
+    shard_check();
+    const size_t rows = (size_t)d_.K + (sh_init_phase_ ? sh_init_ : sh_children_);
+    const size_t nc = rows * d_.pm;
+    ensure_scratch_dbl(std::max(nc, rows));
+    if (cands) {
+      uncast_kernel<S><<<grid_for(nc), 256, 0, stream_>>>(pop_[sh_cur_], scratch_dbl_, nc);
+      CK(cudaMemcpyAsync(cands, scratch_dbl_, sizeof(double) * nc, cudaMemcpyDeviceToHost, stream_));
+      CK(cudaStreamSynchronize(stream_));
+    }
+    if (costs) {
+      uncast_kernel<S><<<grid_for(rows), 256, 0, stream_>>>(cost_[sh_cur_], scratch_dbl_, rows);
+      CK(cudaMemcpyAsync(costs, scratch_dbl_, sizeof(double) * rows, cudaMemcpyDeviceToHost, stream_));
+      CK(cudaStreamSynchronize(stream_));
+    }
+  }
+
   std::string describe() override {
     const Variant<S>& v = pick();
     const Launch a = plan(v, d_.N - d_.K);
@@ -763,6 +872,10 @@ class Engine final : public EngineBase {
   std::vector<Variant<S>> variants_;
   int forced_ = -1;
   int cps_ = 0;  // CTAs per SM for the rollout (0: heuristic)
+  int cand_base_ = 0;  // global index of local candidate 0 (population sharding)
+  long long sh_child_base_ = 0, sh_init_base_ = 0;
+  int sh_children_ = 0, sh_init_ = 0, sh_owns_elites_ = 0, sh_cur_ = 0;
+  bool sh_init_phase_ = true, sh_on_ = false;
   bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
   unsigned long long* dbg_ = nullptr;
   size_t dbg_n_ = 0;
@@ -924,6 +1037,33 @@ int empc_num_variants(empc_handle* h, int32_t* count) {
 int empc_set_variant(empc_handle* h, int32_t variant) { GUARD(h, h->eng->set_variant(variant)); }
 
 int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm) { GUARD(h, h->eng->set_occupancy(ctas_per_sm)); }
+
+int empc_shard_setup(empc_handle* h, int64_t child_base, int32_t n_children, int64_t init_base, int32_t n_init,
+                     int32_t owns_elites) {
+  GUARD(h, h->eng->shard_setup(child_base, n_children, init_base, n_init, owns_elites));
+}
+int empc_shard_entry_bytes(empc_handle* h, int64_t* bytes) {
+  GUARD(h, { if (!bytes) throw InvalidArg{"null"}; *bytes = (int64_t)h->eng->shard_entry_size(); });
+}
+int empc_shard_init(empc_handle* h, const empc_run_args* args) {
+  GUARD(h, { if (!args) throw InvalidArg{"null args"}; h->eng->shard_init(*args); });
+}
+int empc_shard_export(empc_handle* h, void* dev_entries) {
+  GUARD(h, { if (!dev_entries) throw InvalidArg{"null buffer"}; h->eng->shard_export(dev_entries); });
+}
+int empc_shard_import(empc_handle* h, const void* dev_all, int32_t world, double* u_out, double* best_out,
+                      double* best_cost, int64_t* best_row) {
+  GUARD(h, {
+    if (!dev_all || world < 1) throw InvalidArg{"invalid import"};
+    long long g = 0;
+    h->eng->shard_import(dev_all, world, u_out, best_out, best_cost, &g);
+    if (best_row) *best_row = g;
+  });
+}
+int empc_shard_evolve(empc_handle* h, const empc_run_args* args) {
+  GUARD(h, { if (!args) throw InvalidArg{"null args"}; h->eng->shard_evolve(*args); });
+}
+int empc_shard_read(empc_handle* h, double* cands, double* costs) { GUARD(h, h->eng->shard_read(cands, costs)); }
 
 int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out) {
   if (count <= 0) return EMPC_OK;

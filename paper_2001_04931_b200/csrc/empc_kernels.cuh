@@ -51,6 +51,7 @@ struct RolloutArgs {
   int tileP;   // tile rounded up to CC
   int tPS;     // padded candidate stride of the knot / drive buffers
   int evolve;  // index of this evolve within the run (RNG generation = gen0 + evolve)
+  int cand_base;  // global index of candidate 0 of this launch (population sharding; RNG counters)
   const double* prob;   // FP64 problem staging, instances x SL.stride
   const double* state;  // FP64 state staging (x0, sigma), instances x SL.sstride
   const int* idx1;
@@ -268,12 +269,13 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
       // parents (K/empc.py:196): two uniform elite ranks per child
       for (int c = tid; c < cnt; c += nthr) {
         const int child = tile0 + c;
+        const uint32_t gchild = (uint32_t)(a.cand_base + child);
         if (a.mode == kBreedInject) {
           const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
           src[2 * c] = pp[0];
           src[2 * c + 1] = pp[1];
         } else {
-          const U4 r = philox4x32_10(U4{kParentWord, (uint32_t)child, (uint32_t)inst, gen}, key0, key1);
+          const U4 r = philox4x32_10(U4{kParentWord, gchild, (uint32_t)inst, gen}, key0, key1);
           src[2 * c] = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
           src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)d.K);
         }
@@ -288,14 +290,14 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
         bool take = false;
         if (e < tileP * pm && c < cnt) {
           const int l = g % m;
-          const int cand = tile0 + c;
+          const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
           if (philox_breed) {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, gen}, key0, key1);
+            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, gen}, key0, key1);
             take = (uint64_t)r.x < rp.thr_cross;
             const bool mut = (uint64_t)r.y < rp.thr_mut;
             UsT[g * tPS + c] = mut ? normal_bm<S>(r.z, r.w) * csig[l] : S(0);
           } else {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)cand, (uint32_t)inst, kInitTag}, key0, key1);
+            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, kInitTag}, key0, key1);
             const S lo = cumin[l], hi = cumax[l];
             const S v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
             UsT[g * tPS + c] = v > hi ? hi : v;
@@ -746,6 +748,116 @@ __global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
     if (lane == 0 && cnt < K) elite_idx[(size_t)inst * K + cnt] = re;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Population sharding over GPUs: every rank holds the K
+// elites (replicated) and its own slice of the children.  Per generation
+// each rank exports its local top-K candidates as self-contained entries
+// (key, global row, cost, genes); after an all-gather of W x K entries every
+// rank ranks the union identically and installs the global top-K as rows
+// [0, K).  Keys use GLOBAL rows and the RNG counters GLOBAL child indices, so
+// the result equals the unsharded solve for any number of ranks.
+
+template <typename S>
+__host__ __device__ inline size_t shard_entry_bytes(int pm) {
+  return ((size_t)24 + (size_t)pm * sizeof(S) + 15) & ~(size_t)15;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) shard_export_kernel(const S* __restrict__ pop, const S* __restrict__ costs,
+                                                           int K, int pm, int incl_elites, int n_local,
+                                                           long long gbase, unsigned char* __restrict__ out) {
+  using OT = typename OrdOf<S>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int E0 = incl_elites ? K : 0;
+  const int M = E0 + n_local;
+  OT* ck = reinterpret_cast<OT*>(smem_raw);
+  unsigned* cr = reinterpret_cast<unsigned*>(ck + M);  // global rows
+  int* lr = reinterpret_cast<int*>(cr + M);            // local rows
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const size_t eb = shard_entry_bytes<S>(pm);
+  pdl_wait();
+  for (int j = tid; j < M; j += nthr) {
+    const int row = j < E0 ? j : K + (j - E0);
+    lr[j] = row;
+    cr[j] = j < E0 ? (unsigned)j : (unsigned)(gbase + (j - E0));
+    ck[j] = OrdOf<S>::ord(costs[row]);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)  // sentinels when this rank holds fewer than K candidates
+    for (int r = M + tid; r < K; r += nthr) {
+      unsigned char* e = out + (size_t)r * eb;
+      *reinterpret_cast<unsigned long long*>(e) = ~0ull;
+      *reinterpret_cast<unsigned*>(e + 8) = 0xFFFFFFFFu - (unsigned)r;
+      *reinterpret_cast<unsigned*>(e + 12) = 0u;
+    }
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int e0 = blockIdx.x * per, e1 = min(M, e0 + per);
+  for (int e = e0 + warp; e < e1; e += nwarps) {
+    const OT ke = ck[e];
+    const unsigned re = cr[e];
+    int cnt = 0;
+    for (int j = lane; j < M; j += 32) cnt += (ck[j] < ke || (ck[j] == ke && cr[j] < re)) ? 1 : 0;
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (cnt < K) {
+      unsigned char* ent = out + (size_t)cnt * eb;
+      const S* g = pop + (size_t)lr[e] * pm;
+      if (lane == 0) {
+        *reinterpret_cast<unsigned long long*>(ent) = (unsigned long long)ke;
+        *reinterpret_cast<unsigned*>(ent + 8) = re;
+        *reinterpret_cast<unsigned*>(ent + 12) = 1u;
+        *reinterpret_cast<S*>(ent + 16) = costs[lr[e]];
+      }
+      S* dst = reinterpret_cast<S*>(ent + 24);
+      for (int q = lane; q < pm; q += 32) dst[q] = g[q];
+    }
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) shard_import_kernel(const unsigned char* __restrict__ all, int M, int K, int pm,
+                                                           int m, S* __restrict__ pop, S* __restrict__ costs,
+                                                           int* __restrict__ elite_idx, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* ck = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned* cr = reinterpret_cast<unsigned*>(ck + M);
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const size_t eb = shard_entry_bytes<S>(pm);
+  pdl_wait();
+  for (int j = tid; j < M; j += nthr) {
+    ck[j] = *reinterpret_cast<const unsigned long long*>(all + (size_t)j * eb);
+    cr[j] = *reinterpret_cast<const unsigned*>(all + (size_t)j * eb + 8);
+  }
+  __syncthreads();
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int e0 = blockIdx.x * per, e1 = min(M, e0 + per);
+  for (int e = e0 + warp; e < e1; e += nwarps) {
+    const unsigned long long ke = ck[e];
+    const unsigned re = cr[e];
+    int cnt = 0;
+    for (int j = lane; j < M; j += 32) cnt += (ck[j] < ke || (ck[j] == ke && cr[j] < re)) ? 1 : 0;
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (cnt < K) {
+      const unsigned char* ent = all + (size_t)e * eb;
+      const S* g = reinterpret_cast<const S*>(ent + 24);
+      for (int q = lane; q < pm; q += 32) pop[(size_t)cnt * pm + q] = g[q];
+      if (lane == 0) {
+        const S c = *reinterpret_cast<const S*>(ent + 16);
+        costs[cnt] = c;
+        elite_idx[cnt] = cnt;
+        if (cnt == 0) {
+          out[m + pm] = (double)c;
+          out[m + pm + 1] = (double)re;
+        }
+      }
+      if (cnt == 0)
+        for (int q = lane; q < pm; q += 32) {
+          out[m + q] = (double)g[q];
+          if (q < m) out[q] = (double)g[q];
+        }
+    }
   }
 }
 

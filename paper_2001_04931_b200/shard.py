@@ -43,3 +43,144 @@ def gather_instances(local: np.ndarray, total: int, group=None) -> np.ndarray:
     dist.all_gather(outs, t, group=group)
     full = np.concatenate([o.cpu().numpy() for o in outs])[:total]
     return full
+
+
+# ---------------------------------------------------------------------------
+# population sharding (C4: one very large population over W GPUs)
+
+
+class PopulationShard:
+    """One rank's part of a population-sharded ``solve_empc``.
+
+    The rank holds the K elites (replicated) and the children of global child
+    indices ``instance_range(N - K, rank, world)`` (and, for the cold start,
+    the initial candidates ``instance_range(N, rank, world)``).  One exchange
+    per generation: ``export()`` -> all-gather of W x K entries ->
+    ``import_()`` ranks them identically on every rank.  Results equal the
+    unsharded solve bit for bit for any ``world`` (global rows in the
+    selection keys, global child indices in the RNG counters).
+    """
+
+    def __init__(self, spec, sched, settings, rank: int, world: int):
+        import ctypes as C
+
+        from . import _native as nat
+        from .empc import _is_diag, _mutation_sigma, _problem_arrays  # noqa: F401
+        from .param import schedule_arrays
+
+        self.nat, self.C = nat, C
+        self.spec, self.sched, self.settings = spec, sched, settings
+        self.rank, self.world = rank, world
+        N, K = settings.num_sims, settings.num_parents
+        n, m = spec.model.Ad.shape[0], spec.model.Bd.shape[1]
+        self.cb, self.cn = instance_range(N - K, rank, world)
+        self.ib, self.inn = instance_range(N, rank, world)
+        rows = K + max(self.cn, self.inn, 1)
+        self.h = nat.Handle(n, m, spec.T, sched.p, rows, K, 1, not _is_diag(spec.Q),
+                            nat.EMPC_FP64 if settings.precision == "fp64" else nat.EMPC_FP32)
+        i1, i2, c = schedule_arrays(spec.T, sched.p)
+        self.h.call("empc_set_schedule", nat.iptr(np.ascontiguousarray(i1)), nat.iptr(np.ascontiguousarray(i2)),
+                    nat.dptr(np.ascontiguousarray(c)))
+        pa = _problem_arrays(spec)
+        arrs = [nat.f64(pa[k]) for k in ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")]
+        self.h.call("empc_set_problems", 0, 1, *[nat.dptr(x) for x in arrs])
+        self.h.call("empc_shard_setup", self.cb, self.cn, self.ib, self.inn, 1 if rank == 0 else 0)
+        eb = C.c_int64()
+        self.h.call("empc_shard_entry_bytes", C.byref(eb))
+        self.entry_bytes = eb.value
+        self.K, self.m, self.p = K, m, sched.p
+        self._args = nat.empc_run_args()
+
+    def _run_args(self, x0, generation):
+        from .empc import _mutation_sigma
+
+        nat, st = self.nat, self.settings
+        a = self._args
+        self._x0 = nat.f64(np.asarray(x0, float).reshape(1, -1))
+        self._sg = nat.f64(_mutation_sigma(self.spec, st, np.asarray(x0, float))[None])
+        a.init, a.rescore, a.evolves, a.slot_in, a.slot_out = 1, 0, 0, -1, -1
+        a.generation0 = int(generation)
+        a.seed = int(st.seed) & 0xFFFFFFFFFFFFFFFF
+        a.mutation_prob, a.crossover_prob = float(st.mutation_prob), float(st.crossover_prob)
+        a.x0, a.sigma = nat.dptr(self._x0), nat.dptr(self._sg)
+        return a
+
+    def init(self, x0):
+        self.h.call("empc_shard_init", self.C.byref(self._run_args(x0, 1)))
+
+    def export(self, device_ptr: int):
+        """Write this rank's top-K entries (K * entry_bytes) to device memory."""
+        self.h.call("empc_shard_export", self.C.c_void_p(device_ptr))
+
+    def import_(self, device_ptr: int, world: int):
+        nat, C = self.nat, self.C
+        u = np.empty(self.m)
+        best = np.empty((self.p, self.m))
+        cost = np.empty(1)
+        row = C.c_int64()
+        self.h.call("empc_shard_import", C.c_void_p(device_ptr), world, nat.dptr(u), nat.dptr(best), nat.dptr(cost),
+                    C.byref(row))
+        return u, best, float(cost[0]), row.value
+
+    def evolve(self, x0, generation: int):
+        self.h.call("empc_shard_evolve", self.C.byref(self._run_args(x0, generation)))
+
+    def local_population(self):
+        """(candidates, costs) of rows [elites; this rank's children]."""
+        rows = self.K + self.cn
+        c = np.empty((rows, self.p, self.m))
+        k = np.empty(rows)
+        self.h.call("empc_shard_read", self.nat.dptr(c), self.nat.dptr(k))
+        return c, k
+
+
+def solve_population_sharded(shard: PopulationShard, x0, all_gather):
+    """Cold solve of one population split over ranks (K/empc.py:211-236):
+    init + (G-1) x [exchange, select, breed] + a final exchange for the best.
+
+    ``all_gather(local_uint8_tensor) -> gathered_uint8_tensor`` concatenates
+    every rank's export in rank order (e.g. ``dist.all_gather_into_tensor`` over
+    NCCL).  Returns (u, best, best_cost)."""
+    import torch
+
+    K, eb = shard.K, shard.entry_bytes
+    local = torch.empty(K * eb, dtype=torch.uint8, device="cuda")
+    shard.init(x0)
+    for g in range(1, shard.settings.generations):
+        shard.export(local.data_ptr())
+        gathered = all_gather(local)
+        torch.cuda.synchronize()
+        shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb))
+        shard.evolve(x0, g)
+    shard.export(local.data_ptr())
+    gathered = all_gather(local)
+    torch.cuda.synchronize()
+    u, best, cost, _ = shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb))
+    return u, best, cost
+
+
+def solve_population_emulated(spec, sched, settings, x0, world: int):
+    """All ranks of a population-sharded solve in one process on one GPU,
+    stepped in lock-step with an on-device gather (tests / single-GPU boxes)."""
+    import torch
+
+    shards = [PopulationShard(spec, sched, settings, r, world) for r in range(world)]
+    K, eb = shards[0].K, shards[0].entry_bytes
+    bufs = [torch.empty(K * eb, dtype=torch.uint8, device="cuda") for _ in range(world)]
+
+    def exchange():
+        for s, b in zip(shards, bufs):
+            s.export(b.data_ptr())
+        allb = torch.cat(bufs)
+        torch.cuda.synchronize()
+        return [s.import_(allb.data_ptr(), world) for s in shards]
+
+    for s in shards:
+        s.init(x0)
+    for g in range(1, settings.generations):
+        exchange()
+        for s in shards:
+            s.evolve(x0, g)
+    res = exchange()
+    assert all(r[2] == res[0][2] and r[3] == res[0][3] for r in res), "ranks disagree on the best candidate"
+    return res[0], shards

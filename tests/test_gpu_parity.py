@@ -483,3 +483,30 @@ def test_batched_instances_match_individual_solves():
         np.testing.assert_allclose(r.population.costs[i], O.rollout_costs(cands, pr, x0s[i]), rtol=RTOL32)
         assert r.best_cost[i] == pytest.approx(np.min(r.population.costs[i]))
     assert r.u.shape == (5, 3) and r.best.shape == (5, 3, 3)
+
+
+# ---------------------------------------------------------------------------
+# population sharding: any world size gives the unsharded result
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_population_sharding_matches_unsharded(world):
+    from paper_2001_04931_b200 import workloads as W
+    from paper_2001_04931_b200.shard import solve_population_emulated
+
+    spec, x0 = W.nlink_problem(6, 50, 0)
+    sched = P.KnotSchedule(50, 3)
+    st = P.EmpcSettings(num_sims=1024, num_parents=64, generations=5, seed=3)
+    ref = P.solve_empc(spec, sched, st, x0)
+    (u, best, cost, row), shards = solve_population_emulated(spec, sched, st, x0, world)
+    np.testing.assert_array_equal(best, ref.best)
+    np.testing.assert_array_equal(u, ref.u)
+    assert cost == ref.best_cost
+    # after the final exchange every rank holds the top-K of the final population
+    cands, costs = shards[-1].local_population()
+    order = np.argsort(ref.population.costs, kind="stable")[:64]
+    np.testing.assert_array_equal(cands[:64], ref.population.candidates[order])
+    np.testing.assert_array_equal(costs[:64], ref.population.costs[order])
+    # and the union of the children slices is the unsharded children block
+    kids = np.concatenate([s.local_population()[0][64:] for s in shards])
+    np.testing.assert_array_equal(kids, ref.population.candidates[64:])
