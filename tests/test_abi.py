@@ -40,14 +40,16 @@ def test_library_is_sm100a():
 
 
 def test_rollout_kernels_use_fp32_fma():
-    """The rollout hot loop is FFMA work (SURVEY §8d roofline): its SASS is
-    dominated by FFMA and carries no legacy HMMA tensor path."""
+    """The rollout hot loop is FFMA work (SURVEY §8d roofline): the default
+    C3 variant's SASS is dominated by FFMA and carries no legacy HMMA path."""
     if not os.path.exists(nat.LIB_PATH):
         pytest.skip("library not built")
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun",
-                           "_ZN4empc14rollout_kernelIfLi48ELi1ELi4ELb1ELb0ELi1ELi384EEEvNS_11RolloutArgsIT_EE",
-                           nat.LIB_PATH], capture_output=True, text=True).stdout
-    assert sass.count("FFMA") >= 192  # 48 columns x 4 candidates, fully unrolled
+    listing = subprocess.run(["cuobjdump", "-sass", nat.LIB_PATH], capture_output=True, text=True).stdout
+    names = re.findall(r"Function : (_ZN4empc14rollout_kernelIfLi48ELi2ELi4ELb1ELb0ELi2E\S*)", listing)
+    assert names, "default C3 rollout variant (NP48 RR2 CC4 areg ks2) not compiled"
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", names[0], nat.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert sass.count("FFMA") >= 192  # 24 columns x 2 rows x 4 candidates per step, fully unrolled
     assert "HMMA" not in sass
 
 
