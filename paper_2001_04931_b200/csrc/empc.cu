@@ -324,7 +324,9 @@ class Engine final : public EngineBase {
 
   int default_cps(const Variant<S>& v, int nc) const {
     (void)v; (void)nc;
-    return 1;
+    // small single problems are latency bound: several small CTAs per SM
+    // (independent step pipelines) beat one large one (tools/tune.py, C2)
+    return (I_ == 1 && d_.NP <= 16) ? 4 : 1;
   }
 
   // Default variant from measured preferences on B200 (tools/tune.py,
@@ -339,7 +341,12 @@ class Engine final : public EngineBase {
     };
     if (!dense_ && sizeof(S) == 4) {
       const Variant<S>* pref[4] = {nullptr, nullptr, nullptr, nullptr};
-      if (d_.NP <= 48 && I_ == 1) {
+      if (d_.NP <= 8) {
+        pref[0] = find(1, 4, true, 1);
+      } else if (d_.NP <= 16) {
+        pref[0] = find(2, 2, true, 1);
+        pref[1] = find(1, 4, true, 1);
+      } else if (d_.NP <= 48 && I_ == 1) {
         pref[0] = find(2, 4, true, 2);
         pref[1] = find(1, 4, true, 1);
       } else if (d_.NP <= 48) {
@@ -369,6 +376,8 @@ class Engine final : public EngineBase {
     a.nc = nc; a.row0 = row0; a.rows = rows;
     a.tile = L.tile; a.tileP = L.tileP; a.tPS = tps_for(L.tileP); a.evolve = evolve;
     a.cand_base = cand_base_;
+    a.copy_elites = elites_copied_ ? 0 : 1;
+    elites_copied_ = false;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
     a.pop_in = pin; a.cost_in = cin; a.pop_out = pout; a.cost_out = cout;
@@ -414,14 +423,15 @@ class Engine final : public EngineBase {
 
   // evolve index g selects the qualifier-list buffer: rollout g appends to
   // buffer g & 1, selection g + 1 ranks it and clears buffer (g + 1) & 1
-  void launch_select(const S* costs, int incremental = 0, int g = 0) {
+  void launch_select(const S* costs, int incremental = 0, int g = 0, const S* pop_in = nullptr, S* pop_out = nullptr,
+                     S* cost_out = nullptr) {
     const int N = d_.N;
     const int ctas = I_ == 1 ? std::max(1, std::min(sms_, (N + 15) / 16)) : 1;
     int* qin = incremental ? qcount_ + (size_t)((g - 1) & 1) * I_ : nullptr;
     const void* lin = (const char*)qlist_ + (size_t)((g - 1) & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
     int* qnext = qcount_ + (size_t)(g & 1) * I_;
     launch_ex(select_kernel<S>, dim3(ctas, I_), dim3(256), select_smem_, pdl_next_, costs, N, d_.K, elite_, incremental,
-              qin, lin, qnext, qcap_);
+              qin, lin, qnext, qcap_, pop_in, pop_out, cost_out, d_.pm);
     pdl_next_ = use_pdl_;
     ++launches_;
   }
@@ -456,7 +466,8 @@ class Engine final : public EngineBase {
     const int nc = d_.N - d_.K;
     for (int g = 0; g < r.evolves; ++g) {
       // after the first evolve of a run, rows [0, K) hold the sorted elites
-      launch_select(cost_[cur], (g > 0 && incremental_) ? 1 : 0, g);
+      launch_select(cost_[cur], (g > 0 && incremental_) ? 1 : 0, g, pop_[cur], pop_[cur ^ 1], cost_[cur ^ 1]);
+      elites_copied_ = true;
       const int* par = nullptr;
       const uint8_t *tk = nullptr, *mu = nullptr;
       const double* nz = nullptr;
@@ -873,6 +884,7 @@ class Engine final : public EngineBase {
   int forced_ = -1;
   int cps_ = 0;  // CTAs per SM for the rollout (0: heuristic)
   int cand_base_ = 0;  // global index of local candidate 0 (population sharding)
+  bool elites_copied_ = false;  // the last selection also carried the elites over
   long long sh_child_base_ = 0, sh_init_base_ = 0;
   int sh_children_ = 0, sh_init_ = 0, sh_owns_elites_ = 0, sh_cur_ = 0;
   bool sh_init_phase_ = true, sh_on_ = false;

@@ -52,6 +52,7 @@ struct RolloutArgs {
   int tPS;     // padded candidate stride of the knot / drive buffers
   int evolve;  // index of this evolve within the run (RNG generation = gen0 + evolve)
   int cand_base;  // global index of candidate 0 of this launch (population sharding; RNG counters)
+  int copy_elites;  // 1: this launch copies the elite rows (0 when the selection kernel did)
   const double* prob;   // FP64 problem staging, instances x SL.stride
   const double* state;  // FP64 state staging (x0, sigma), instances x SL.sstride
   const int* idx1;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   EMPC_MARK(2)
   // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
   // population are the sorted elites with their carried costs.
-  if (breed) {
+  if (breed && a.copy_elites) {  // otherwise the selection kernel already did
     for (int e = blockIdx.x; e < d.K; e += gridDim.x) {
       const int s = a.elite_idx[(size_t)inst * d.K + e];
       const S* from = a.pop_in + (pop_base + s) * pm;
@@ -705,7 +706,9 @@ template <typename S>
 __global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs, int N, int K,
                                                      int* __restrict__ elite_idx, int incremental,
                                                      int* __restrict__ qcount_in, const void* __restrict__ qlist_in,
-                                                     int* __restrict__ qcount_next, int qcap) {
+                                                     int* __restrict__ qcount_next, int qcap,
+                                                     const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                                     S* __restrict__ cost_out, int pm) {
   using OT = typename OrdOf<S>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OT* ck = reinterpret_cast<OT*>(smem_raw);
@@ -747,7 +750,17 @@ __global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs
       cnt += (kj < ke || (kj == ke && ci[j] < re)) ? 1 : 0;
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-    if (lane == 0 && cnt < K) elite_idx[(size_t)inst * K + cnt] = re;
+    if (cnt < K) {
+      if (lane == 0) elite_idx[(size_t)inst * K + cnt] = re;
+      if (pop_out != nullptr) {
+        // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
+        // population are the sorted elites with their carried costs
+        const S* from = pop_in + ((size_t)inst * N + re) * pm;
+        S* to = pop_out + ((size_t)inst * N + cnt) * pm;
+        for (int g = lane; g < pm; g += 32) to[g] = from[g];
+        if (lane == 0) cost_out[(size_t)inst * N + cnt] = c[re];
+      }
+    }
   }
 }
 
