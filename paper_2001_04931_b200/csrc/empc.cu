@@ -105,6 +105,8 @@ class Engine final : public EngineBase {
     if (const char* v = std::getenv("EMPC_VARIANT")) forced_ = std::atoi(v);
     phases_ = std::getenv("EMPC_PHASES") != nullptr;
     incremental_ = std::getenv("EMPC_FULL_SELECT") == nullptr;
+    persist_enabled_ = std::getenv("EMPC_NO_PERSIST") == nullptr;
+    persist_ = persist_variants<S>();
     if (phases_) {
       dbg_n_ = (size_t)1 << 20;
       CK(cudaMalloc(&dbg_, dbg_n_ * 8));
@@ -283,7 +285,7 @@ class Engine final : public EngineBase {
     return t;
   }
 
-  Launch plan(const Variant<S>& v, int nc) const {
+  Launch plan(const Variant<S>& v, int nc, int cps_override = 0) const {
     const int NRG = v.NP / v.RR;
     const int CC = v.CC;
     auto threads_for = [&](int tileP) {
@@ -303,7 +305,7 @@ class Engine final : public EngineBase {
     } else if (I_ == 1 || cps_ > 0) {
       // one wave of `cps` CTAs per SM: small CTAs synchronise only their own
       // warps each step, so the SM interleaves independent step pipelines
-      const int cps = std::max(1, cps_ > 0 ? cps_ : default_cps(v, nc));
+      const int cps = std::max(1, cps_override > 0 ? cps_override : (cps_ > 0 ? cps_ : default_cps(v, nc)));
       int tile = (nc + sms_ * cps - 1) / (sms_ * cps);
       if (tile > maxP) tile = maxP;        // several waves when smem / threads limit the tile
       int tiles = (nc + tile - 1) / tile;
@@ -436,6 +438,80 @@ class Engine final : public EngineBase {
     ++launches_;
   }
 
+  // Persistent cooperative path (single instance, default variant, every
+  // tile co-resident): the whole run is one launch.  Returns false when the
+  // configuration does not qualify and the per-generation launches are used.
+  template <typename Pre, typename Post>
+  bool try_persistent(const empc_run_args& r, bool timed, Pre& pre, Post& post) {
+    if (!persist_enabled_ || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K)
+      return false;
+    const Variant<S>& v = pick();
+    const PersistVariant<S>* pv = nullptr;
+    for (auto& p : persist_)
+      if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws) pv = &p;
+    if (!pv) return false;
+    const int nc = d_.N - d_.K;
+    const Launch Le = plan(v, nc, 1);
+    if (Le.tiles > sms_) return false;
+    const int grid = Le.tiles;
+    const int tile0 = (d_.N + grid - 1) / grid;
+    const int tileP = (std::max(tile0, Le.tile) + v.CC - 1) / v.CC * v.CC;
+    const int NRG = v.NP / v.RR;
+    const int nl = NRG * (tileP / v.CC);
+    const int threads = v.ks == 1 ? (nl + 31) / 32 * 32 : 2 * ((nl + 15) / 16 * 16);
+    if (threads > v.maxt) return false;
+    const size_t smem =
+        smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq, select_smem_).total;
+    if (smem > (size_t)kMaxSmem - 1024) return false;
+    if (!persist_attr_set_) {
+      for (auto& p : persist_)
+        CK(cudaFuncSetAttribute(p.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+      persist_attr_set_ = true;
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pv->kernel, threads, smem));
+    if (per_sm * sms_ < grid) return false;
+    PersistArgs<S> P{};
+    RolloutArgs<S>& a = P.ro;
+    a.d = d_; a.SL = SL_; a.r_diag = r_diag_ ? 1 : 0;
+    a.mode = r.init ? kInitPhilox : kScore;
+    a.nc = d_.N; a.row0 = 0; a.rows = d_.N;
+    a.tile = tile0; a.tileP = tileP; a.tPS = tps_for(tileP); a.evolve = 0; a.cand_base = 0; a.copy_elites = 0;
+    a.prob = stage_prob_d_; a.state = stage_state_d_;
+    a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
+    a.pop_in = pop_[0]; a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
+    a.elite_idx = elite_; a.run = run_d_;
+    a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
+    P.evolves = r.evolves;
+    P.tile_evolve = Le.tile;
+    P.incremental = incremental_ ? 1 : 0;
+    P.scratch = select_smem_;
+    P.pop[0] = pop_[0]; P.pop[1] = pop_[1];
+    P.cost[0] = cost_[0]; P.cost[1] = cost_[1];
+    P.qcount = qcount_;
+    P.qlist = qlist_;
+    P.elite = elite_;
+    P.out = out_d_;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream_;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (timed) pre();
+    CK(cudaLaunchKernelEx(&cfg, pv->kernel, P));
+    ++launches_;
+    ++rollout_launches_;
+    if (timed) post();
+    persist_desc_ = std::string("persistent grid=") + std::to_string(grid) + " threads=" + std::to_string(threads) +
+                    " smem=" + std::to_string(smem);
+    return true;
+  }
+
   // The device part of a run: prep, optional init / rescore, evolves, finalize.
   // Returns the index (0/1) of the buffer holding the final population.
   int enqueue_core(const empc_run_args& r, const std::vector<const void*>* inj, bool timed_rollouts = false) {
@@ -452,6 +528,7 @@ class Engine final : public EngineBase {
     auto post = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_ - 1], stream_)); };
     int cur = 0;
     const size_t pm = d_.pm;
+    if (inj == nullptr && try_persistent(r, timed_rollouts, pre, post)) return r.evolves & 1;
     if (r.init) {
       const S* inj_init = inj ? (const S*)(*inj)[0] : nullptr;
       pre();
@@ -819,8 +896,9 @@ class Engine final : public EngineBase {
     const Variant<S>& v = pick();
     const Launch a = plan(v, d_.N - d_.K);
     char buf[512];
-    std::snprintf(buf, sizeof buf, "%s | evolve tile=%d tileP=%d tiles=%d threads=%d smem=%zu | sms=%d", v.name, a.tile,
-                  a.tileP, a.tiles, a.threads, a.smem, sms_);
+    std::snprintf(buf, sizeof buf, "%s | evolve tile=%d tileP=%d tiles=%d threads=%d smem=%zu | sms=%d%s%s", v.name,
+                  a.tile, a.tileP, a.tiles, a.threads, a.smem, sms_, persist_desc_.empty() ? "" : " | ",
+                  persist_desc_.c_str());
     return buf;
   }
   int num_variants() override { return (int)variants_.size(); }
@@ -889,6 +967,9 @@ class Engine final : public EngineBase {
   int sh_children_ = 0, sh_init_ = 0, sh_owns_elites_ = 0, sh_cur_ = 0;
   bool sh_init_phase_ = true, sh_on_ = false;
   bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
+  bool persist_enabled_ = true, persist_attr_set_ = false;
+  std::vector<PersistVariant<S>> persist_;
+  std::string persist_desc_;
   unsigned long long* dbg_ = nullptr;
   size_t dbg_n_ = 0;
   int dbg_ctas_ = 0;

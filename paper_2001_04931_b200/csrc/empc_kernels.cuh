@@ -11,6 +11,7 @@
 //   expand_kernel   K1: knots -> per-step inputs (K/param.py:114-116)
 #pragma once
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "empc_device.cuh"
@@ -94,11 +95,15 @@ struct Geo {
 
 // Shared memory plan (host and device agree on it).
 struct SmemPlan {
-  size_t us, but, xc, as, qs, sched, g, cu, src, cv, total;
+  size_t us, but, xc, as, qs, sched, g, cu, src, cv, bs, total;
 };
 
 template <typename S>
-__host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int tileP, int tPS, bool areg, bool dq) {
+__host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int tileP, int tPS, bool areg, bool dq,
+                                              size_t persist_scratch = 0) {
+  // persist_scratch > 0: persistent solve -- B gets its own region (it is
+  // reused every generation) and the leading scratch (UsT, BUT, XC) is at
+  // least persist_scratch bytes (the in-kernel selection's key arrays)
   auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
   const int NPS = Geo<S>::nps(NP);
   (void)areg;
@@ -106,7 +111,9 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.us = al((size_t)p * m * tPS * sizeof(S));
   s.but = al((size_t)p * NP * tPS * sizeof(S));
   const size_t xc = (size_t)2 * tileP * NPS, bs = (size_t)NP * (m + 1);
-  s.xc = al((xc > bs ? xc : bs) * sizeof(S));
+  s.xc = al(((persist_scratch || xc > bs) ? xc : bs) * sizeof(S));
+  if (persist_scratch && s.us + s.but + s.xc < persist_scratch) s.xc += al(persist_scratch - (s.us + s.but + s.xc));
+  s.bs = persist_scratch ? al(bs * sizeof(S)) : 0;
   s.as = al((size_t)NP * NPS * sizeof(S));  // A staging (copied to registers by AREG variants)
   s.qs = dq ? al((size_t)NP * NPS * sizeof(S)) : 0;
   s.sched = al((size_t)T * (2 * sizeof(int) + sizeof(S)));
@@ -114,7 +121,7 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
   s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S) + (size_t)((tileP * p * m + 31) / 32 + 1) * 4);
-  s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv;
+  s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv + s.bs;
   return s;
 }
 
@@ -142,8 +149,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // (1) wait for the producer, elite carry-over and breeding; (2) B at the
 // knots and the knot-space input cost; (3) the horizon recursion.
 
-template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a) {
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS>
+__device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage, size_t persist_scratch) {
   constexpr int NRG = NP / RR;
   constexpr int VEC = Geo<S>::VEC;
   constexpr int NPS = Geo<S>::nps(NP);
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   const double* __restrict__ P = a.prob + (size_t)inst * SL.stride;
   const double* __restrict__ X = a.state + (size_t)inst * SL.sstride;
 
-  const SmemPlan sp = smem_plan<S>(NP, m, T, p, tileP, tPS, AREG, DQ);
+  const SmemPlan sp = smem_plan<S>(NP, m, T, p, tileP, tPS, AREG, DQ, persist_scratch);
   unsigned char* ptr = smem_raw;
   S* UsT = reinterpret_cast<S*>(ptr); ptr += sp.us;   // [gene][tPS]
   S* BUT = reinterpret_cast<S*>(ptr); ptr += sp.but;  // [knot][row][tPS]
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   S* sG = reinterpret_cast<S*>(ptr); ptr += sp.g;     // [p*p] + cost0
   S* cU = reinterpret_cast<S*>(ptr); ptr += sp.cu;
   int* src = reinterpret_cast<int*>(ptr); ptr += sp.src;
-  S* cw_ = reinterpret_cast<S*>(ptr);                 // w, qd, xg, x0 [NP]; ug, umin, umax, sig, rdiag [m]
+  S* cw_ = reinterpret_cast<S*>(ptr); ptr += sp.cv;   // w, qd, xg, x0 [NP]; ug, umin, umax, sig, rdiag [m]
   S* cqd = cw_ + NP;
   S* cxg = cqd + NP;
   S* cx0 = cxg + NP;
@@ -186,14 +193,15 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   S* cumax = cumin + m;
   S* csig = cumax + m;
   S* crd = csig + m;
-  S* Bs = XC;
+  S* Bs = persist_scratch ? reinterpret_cast<S*>(ptr) : XC;  // [NP][m+1]
 
   const size_t pop_base = (size_t)inst * a.rows;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
 
   EMPC_MARK(0)
-  // ---- phase 0: problem -> smem (coalesced, all loads in flight together)
-  if (cnt > 0) {
+  // ---- phase 0: problem -> smem (coalesced, all loads in flight together);
+  // a persistent CTA stages even when its first tile is empty (later ones are not)
+  if (stage && (cnt > 0 || persist_scratch)) {
     for (int k = tid; k < T; k += nthr) {
       sI1[k] = a.idx1[k];
       sI2[k] = a.idx2[k];
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
   EMPC_MARK(7)
   __syncthreads();  // phase-0 smem (bounds, sigma) is read by every thread below
   // w += Delta x_goal (error coordinates): one warp per row group, lanes over columns
-  for (int i = warp; i < n; i += nwarps) {
+  for (int i = warp; i < (stage ? n : 0); i += nwarps) {
     S acc = S(0);
     for (int j = lane; j < n; j += 32) acc = fma(As[i * NPS + j], cxg[j], acc);
 #pragma unroll
@@ -284,7 +292,9 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
     }
     if (philox_breed || a.mode == kInitPhilox) {
       // crossover bit + mutation offset (K/empc.py:197-199), or the uniform
-      // initial knot (K/empc.py:170), per gene into UsT
+      // initial knot (K/empc.py:170), per gene into UsT; unrolled so several
+      // independent Philox chains are in flight per thread
+#pragma unroll 4
       for (int e0 = 0; e0 < tileP * pm; e0 += nthr) {
         const int e = e0 + tid;
         const int c = e / pm, g = e - (e / pm) * pm;
@@ -668,6 +678,11 @@ __global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a
 #undef EMPC_MATVEC
 }
 
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) rollout_kernel(const RolloutArgs<S> a) {
+  rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(a, true, 0);
+}
+
 // ---------------------------------------------------------------------------
 // K4 selection: stable top-K (argsort(kind="stable")[:K], K/empc.py:185-186).
 // Key of candidate i = (ord(cost_i), i) -- unique, so the stable order is the
@@ -703,12 +718,11 @@ __host__ __device__ inline size_t select_smem(int N) {
 }
 
 template <typename S>
-__global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs, int N, int K,
-                                                     int* __restrict__ elite_idx, int incremental,
-                                                     int* __restrict__ qcount_in, const void* __restrict__ qlist_in,
-                                                     int* __restrict__ qcount_next, int qcap,
-                                                     const S* __restrict__ pop_in, S* __restrict__ pop_out,
-                                                     S* __restrict__ cost_out, int pm) {
+__device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
+                                            int incremental, int* __restrict__ qcount_in,
+                                            const void* __restrict__ qlist_in, int* __restrict__ qcount_next, int qcap,
+                                            const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                            S* __restrict__ cost_out, int pm) {
   using OT = typename OrdOf<S>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OT* ck = reinterpret_cast<OT*>(smem_raw);
@@ -762,6 +776,17 @@ __global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs
       }
     }
   }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs, int N, int K,
+                                                     int* __restrict__ elite_idx, int incremental,
+                                                     int* __restrict__ qcount_in, const void* __restrict__ qlist_in,
+                                                     int* __restrict__ qcount_next, int qcap,
+                                                     const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                                     S* __restrict__ cost_out, int pm) {
+  select_body<S>(costs, N, K, elite_idx, incremental, qcount_in, qlist_in, qcount_next, qcap, pop_in, pop_out,
+                 cost_out, pm);
 }
 
 // ---------------------------------------------------------------------------
@@ -879,9 +904,8 @@ __global__ void __launch_bounds__(256) shard_import_kernel(const unsigned char* 
 // best candidate, written as FP64 [u (m) | best (pm) | cost | index].
 
 template <typename S>
-__global__ void finalize_kernel(const S* __restrict__ cands, const S* __restrict__ costs, int N, int m, int pm,
-                                double* __restrict__ out) {
-  const int inst = blockIdx.x;
+__device__ __forceinline__ void finalize_body(const S* __restrict__ cands, const S* __restrict__ costs, int N, int m,
+                                              int pm, double* __restrict__ out, int inst) {
   const S* c = costs + (size_t)inst * N;
   pdl_wait();
   uint64_t bo = ~0ull;
@@ -924,6 +948,12 @@ __global__ void finalize_kernel(const S* __restrict__ cands, const S* __restrict
     o[m + pm] = (double)c[best];
     o[m + pm + 1] = (double)best;
   }
+}
+
+template <typename S>
+__global__ void finalize_kernel(const S* __restrict__ cands, const S* __restrict__ costs, int N, int m, int pm,
+                                double* __restrict__ out) {
+  finalize_body<S>(cands, costs, N, m, pm, out, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -972,5 +1002,65 @@ __global__ void philox_kernel(const uint32_t* ctr, const uint32_t* key, int coun
 }
 
 #endif  // EMPC_HOST_TU
+
+// ---------------------------------------------------------------------------
+// Persistent cooperative solve (single instance, all tiles co-resident): the
+// whole cold / warm solve of K/empc.py:211-236 in one launch.  The problem is
+// staged into shared memory (and A into registers) once; each generation is
+//   grid.sync -> distributed selection (select_body) -> grid.sync ->
+//   breed + rollout of this CTA's tile (rollout_body)
+// and the argmin runs on CTA 0 after the last generation.  Same kernels'
+// arithmetic as the per-launch path, so results are identical to it.
+
+template <typename S>
+struct PersistArgs {
+  RolloutArgs<S> ro;  // init / rescore launch of generation 0 (the rest is derived)
+  int evolves;
+  int tile_evolve;    // candidates per CTA for the evolves (tile for gen 0 is ro.tile)
+  int incremental;
+  size_t scratch;     // leading shared-memory bytes the selection needs
+  S* pop[2];
+  S* cost[2];
+  int* qcount;        // [2] double-buffered qualifier counts
+  void* qlist;        // [2][qcap] (key, row) pairs
+  int* elite;         // elite_idx (written by the selection)
+  double* out;
+};
+
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  RolloutArgs<S> a = P.ro;
+  const int N = a.d.N, K = a.d.K, pm = a.d.pm;
+  using OT = typename std::conditional<sizeof(S) == 4, uint32_t, uint64_t>::type;
+  const size_t qstride = (size_t)a.qcap * 2 * sizeof(OT);
+  rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(a, true, P.scratch);
+  int cur = 0;
+  for (int g = 0; g < P.evolves; ++g) {
+    grid.sync();
+    const int inc = (g > 0 && P.incremental) ? 1 : 0;
+    select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+                   (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
+                   P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+    grid.sync();
+    RolloutArgs<S> b = a;
+    b.mode = kBreedPhilox;
+    b.nc = N - K;
+    b.row0 = K;
+    b.tile = P.tile_evolve;
+    b.evolve = g;
+    b.copy_elites = 0;
+    b.pop_in = P.pop[cur];
+    b.cost_in = P.cost[cur];
+    b.pop_out = P.pop[cur ^ 1];
+    b.cost_out = P.cost[cur ^ 1];
+    b.qcount = P.incremental ? P.qcount + (g & 1) : nullptr;
+    b.qlist = (char*)P.qlist + (g & 1) * qstride;
+    rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(b, false, P.scratch);
+    cur ^= 1;
+  }
+  grid.sync();
+  if (blockIdx.x == 0) finalize_body<S>(P.pop[cur], P.cost[cur], N, a.d.m, pm, P.out, 0);
+}
 
 }  // namespace empc

@@ -1,0 +1,23 @@
+// Persistent cooperative solve kernels for the default single-instance FP32
+// variants (see persist_kernel in empc_kernels.cuh).
+#include "empc_variants.h"
+
+namespace empc {
+
+#define PK(NP, RR, CC, AR, KS)                                                                             \
+  PersistVariant<float>{NP, RR, CC, AR, KS,                                                              \
+                        &persist_kernel<float, NP, RR, CC, AR, false, KS, false,                         \
+                                        maxt_for(NP, RR, CC, AR, sizeof(float), KS)>}
+
+template <>
+std::vector<PersistVariant<float>> persist_variants<float>() {
+  return {PK(4, 1, 4, true, 1),  PK(8, 1, 4, true, 1),  PK(12, 2, 2, true, 1), PK(16, 2, 2, true, 1),
+          PK(24, 2, 4, true, 2), PK(32, 2, 4, true, 2), PK(48, 2, 4, true, 2), PK(48, 1, 4, true, 1)};
+}
+
+template <>
+std::vector<PersistVariant<double>> persist_variants<double>() {
+  return {};
+}
+
+}  // namespace empc

@@ -38,4 +38,15 @@ constexpr int maxt_for(int NP, int RR, int CC, bool areg, int elem, int KS) {
 template <typename S>
 std::vector<Variant<S>> variants_for(int NP);
 
+template <typename S>
+struct PersistVariant {
+  int NP, RR, CC;
+  bool areg;
+  int ks;
+  void (*kernel)(const PersistArgs<S>);
+};
+
+template <typename S>
+std::vector<PersistVariant<S>> persist_variants();
+
 }  // namespace empc
