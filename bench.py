@@ -363,7 +363,9 @@ def run_ours(args):
         "latency_ms": {"median": statistics.median(ms_each), "q1": float(np.percentile(ms_each, 25)),
                        "q3": float(np.percentile(ms_each, 75)), "min": min(ms_each)},
         "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "rollout_kernel",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "persist_kernel (whole solve in one cooperative launch: rollouts + selection)"
+                     if "persistent" in ctx.h.describe() else "rollout_kernel",
                      "rollout_ms_per_launch": rollout_ms, "rollout_launches_per_step": nroll,
                      "flop_per_launch": flop_per_launch, "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

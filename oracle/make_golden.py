@@ -146,5 +146,42 @@ def main():
     print("wrote", sorted(os.listdir(OUT)))
 
 
+def closed_loop():
+    """Closed-loop EMPC traces (K/closedloop.py:59-133) for the f1 parity
+    test: the pendulum smoke case of TST/test_closedloop.py:234-245, the same
+    with gravity (the relinearization matters), and a 2-link arm."""
+    sys.path.insert(0, REF)
+    from knotmpc import closedloop as cl, condense, dynamics
+
+    def template(plant, T, umax):
+        clin = dynamics.linearize(plant.ode, np.zeros(plant.n), np.zeros(plant.m))
+        nj = plant.m
+        return condense.MpcSpec(dynamics.discretize(clin, 0.01), T, Q=np.diag([10.0] * nj + [0.1] * nj),
+                                R=0.01 * np.eye(nj), x_goal=np.zeros(plant.n), u_goal=np.zeros(nj),
+                                u_min=-umax * np.ones(nj), u_max=umax * np.ones(nj))
+
+    cases = {
+        "pend0": (dynamics.Pendulum(dynamics.PendulumParams(gravity=0.0)), 30, 25.0, 3, [0.4, 0.0],
+                  dict(num_sims=64, num_parents=8, generations=2), 0.5),
+        "pendg": (dynamics.Pendulum(dynamics.PendulumParams()), 30, 25.0, 3, [0.8, 0.0],
+                  dict(num_sims=128, num_parents=16, generations=3, seed=5), 0.3),
+        "arm2": (dynamics.NLinkArm(dynamics.NLinkParams(links=2)), 20, 2.0, 3, [0.5, -0.3, 0.0, 0.0],
+                 dict(num_sims=256, num_parents=16, generations=3, seed=2), 0.2),
+    }
+    for name, (plant, T, umax, p, goal, st, dur) in cases.items():
+        tpl = template(plant, T, umax)
+        ctl = cl.Controller("empc", p=p, empc=cl.EmpcSettings(**st))
+        res = cl.run_closed_loop(plant, ctl, tpl, x0=np.zeros(plant.n), x_goal=np.array(goal), duration=dur,
+                                 rate=100.0)
+        np.savez_compressed(os.path.join(OUT, f"closedloop_{name}.npz"), states=res.states, inputs=res.inputs,
+                            goal=np.array(goal), T=np.int64(T), umax=umax, p=np.int64(p), duration=dur,
+                            **{"st_" + k: v for k, v in st.items()})
+    print("wrote closed-loop fixtures")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["closedloop"]:
+        closed_loop()
+    else:
+        main()
+        closed_loop()

@@ -2,7 +2,18 @@
 EMPC / knot-parameterization names of the reference package ``knotmpc``
 (K/__init__.py:68-85)."""
 
-from .dynamics import ContinuousLinearModel, DiscreteLinearModel, NLinkArm, NLinkParams, discretize, linearize
+from .closedloop import ClosedLoopFleet, Controller, SimResult, actual_cost, compute_metrics, run_closed_loop
+from .dynamics import (
+    ContinuousLinearModel,
+    DiscreteLinearModel,
+    NLinkArm,
+    NLinkParams,
+    Pendulum,
+    PendulumParams,
+    discretize,
+    integrate,
+    linearize,
+)
 from .empc import (
     BatchResult,
     CostModel,
@@ -30,7 +41,8 @@ from .spec import MpcSpec
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchResult", "ContinuousLinearModel", "CostModel", "DiscreteLinearModel", "EmpcBatch", "EmpcResult",
+    "BatchResult", "ClosedLoopFleet", "Controller", "Pendulum", "PendulumParams", "SimResult", "actual_cost",
+    "compute_metrics", "integrate", "run_closed_loop", "ContinuousLinearModel", "CostModel", "DiscreteLinearModel", "EmpcBatch", "EmpcResult",
     "EmpcSettings", "KnotSchedule", "KnotTrajectory", "MpcSpec", "NLinkArm", "NLinkParams", "Population",
     "discretize", "evaluate_cost", "evolve_generation", "expand", "expand_batch", "init_population", "input_at",
     "interp_coeffs", "interpolation_matrix", "knot_spacing", "linearize", "solve_empc",

@@ -1,10 +1,10 @@
-"""Host-side model types and the synthetic-system generator.
+"""Host-side model types, plants and the synthetic-system generator.
 
-Mirrors the parts of knotmpc.dynamics (K/dynamics.py) the EMPC path consumes:
-``DiscreteLinearModel`` (K/dynamics.py:223-238), plus the model *generation*
-used to build benchmark workloads the way the reference harness does
-(``NLinkArm`` K/dynamics.py:90-199, ``linearize`` K/dynamics.py:241-262,
-``discretize`` K/dynamics.py:265-290).  Model generation is host FP64 work
+Mirrors the parts of knotmpc.dynamics (K/dynamics.py) the EMPC path and its
+closed loop consume: ``DiscreteLinearModel`` (K/dynamics.py:223-238), the
+plants (``Pendulum`` K/dynamics.py:33-75, ``NLinkArm`` K/dynamics.py:90-199),
+``linearize`` (K/dynamics.py:241-262), ``discretize`` (K/dynamics.py:265-290)
+and the RK4 ground-truth integrator (K/dynamics.py:316-330).  Model generation is host FP64 work
 outside the timed solve, exactly as in the paper and the
 reference harness (K/closedloop.py:76-79).
 """
@@ -154,3 +154,56 @@ def discretize(model: ContinuousLinearModel, dt: float, method: str = "exact") -
     aug[:n, -1] = model.w
     E = expm(aug * dt)
     return DiscreteLinearModel(E[:n, :n], E[:n, n:n + m], E[:n, -1], dt)
+
+
+@dataclass(frozen=True)
+class PendulumParams:
+    """m l^2 qdd + b qd + m g l sin(q) = tau, q from the hanging position
+    (K/dynamics.py:33-48)."""
+
+    mass: float = 1.0
+    length: float = 1.0
+    damping: float = 0.05
+    gravity: float = 9.81
+
+    def __post_init__(self):
+        if self.mass <= 0 or self.length <= 0:
+            raise ValueError("mass and length must be positive")
+        if self.damping < 0:
+            raise ValueError("damping must be non-negative")
+
+
+class Pendulum:
+    """Single-joint plant, state [q, qd], one torque input (K/dynamics.py:59-75)."""
+
+    n = 2
+    m = 1
+
+    def __init__(self, params: PendulumParams = PendulumParams()):
+        self.params = params
+
+    def ode(self, x, u):
+        p = self.params
+        q, qd = float(x[0]), float(x[1])
+        inertia = p.mass * p.length**2
+        qdd = (float(u[0]) - p.damping * qd - p.mass * p.gravity * p.length * np.sin(q)) / inertia
+        return np.array([qd, qdd])
+
+
+def rk4_step(f, x, u, dt: float) -> np.ndarray:
+    """Classic RK4 with the input held over the step (K/dynamics.py:316-322)."""
+    h2 = 0.5 * dt
+    k1 = f(x, u)
+    k2 = f(x + h2 * k1, u)
+    k3 = f(x + h2 * k2, u)
+    k4 = f(x + dt * k3, u)
+    return x + (dt / 6.0) * (k1 + 2 * k2 + 2 * k3 + k4)
+
+
+def integrate(f, x, u, dt: float, substeps: int = 10) -> np.ndarray:
+    """One zero-order-hold control period as ``substeps`` RK4 steps
+    (K/dynamics.py:325-330)."""
+    h = dt / substeps
+    for _ in range(substeps):
+        x = rk4_step(f, x, u, h)
+    return x

@@ -1,0 +1,206 @@
+"""Closed-loop EMPC (K/closedloop.py:59-133).
+
+CPU: response metrics against closed forms (the oracles of
+TST/test_closedloop.py), controller validation, and the host loop (relinearize,
+discretize, warm start, clip, RK4) with the oracle standing in for the GPU
+solve, against closed-loop traces recorded from the real reference
+(tests/golden/closedloop_*.npz, oracle/make_golden.py:closed_loop).
+
+GPU: the same traces through the CUDA path (FP64 device mode, the
+reference's random tensors replayed), the reference's EMPC smoke case with
+the in-kernel RNG, and the batched fleet.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2001_04931_b200 as P
+from paper_2001_04931_b200 import closedloop as CL
+from paper_2001_04931_b200 import dynamics as D
+from oracle import empc_oracle as O
+from tests import golden as G
+
+SECOND_ORDER_OVERSHOOT = 16.303353482158048  # zeta=0.5: 100 exp(-pi zeta / sqrt(1-zeta^2))
+EXP_ITAE = 0.9595723180054871  # int_0^5 t exp(-t) dt = 1 - 6 exp(-5)
+
+
+def _template(plant, T, umax):
+    clin = D.linearize(plant.ode, np.zeros(plant.n), np.zeros(plant.m))
+    nj = plant.m
+    return P.MpcSpec(D.discretize(clin, 0.01), T, Q=np.diag([10.0] * nj + [0.1] * nj), R=0.01 * np.eye(nj),
+                     x_goal=np.zeros(plant.n), u_goal=np.zeros(nj), u_min=-umax * np.ones(nj),
+                     u_max=umax * np.ones(nj))
+
+
+CASES = {
+    "pend0": lambda: D.Pendulum(D.PendulumParams(gravity=0.0)),
+    "pendg": lambda: D.Pendulum(D.PendulumParams()),
+    "arm2": lambda: D.NLinkArm(D.NLinkParams(links=2)),
+}
+
+
+def _case(name, **extra):
+    g = G.load("closedloop_" + name)
+    plant = CASES[name]()
+    st = {k[3:]: int(v) for k, v in g.items() if k.startswith("st_")}
+    settings = P.EmpcSettings(**st, **extra)
+    tpl = _template(plant, int(g["T"]), float(g["umax"]))
+    ctl = CL.Controller("empc", p=int(g["p"]), empc=settings)
+    return g, plant, tpl, ctl
+
+
+def _replay(settings, p, umin, umax):
+    """The reference's random tensors for a solve starting at generation g0."""
+    ost = O.Settings.from_settings(settings)
+
+    def fn(g0, evolves, cold):
+        init = O.rng(ost.seed, 0).uniform(umin, umax, size=(ost.num_sims, p, len(umin))) if cold else None
+        return init, [O.draws(ost, g, p, len(umin)) for g in range(g0, g0 + evolves)]
+
+    return fn
+
+
+# ---------------------------------------------------------------------------
+# metrics (CPU)
+
+
+def test_metrics_second_order_overshoot():
+    zeta, wn = 0.5, 2.0
+    t = np.linspace(0, 10, 100001)
+    wd = wn * np.sqrt(1 - zeta**2)
+    y = 1 - np.exp(-zeta * wn * t) * (np.cos(wd * t) + zeta / np.sqrt(1 - zeta**2) * np.sin(wd * t))
+    assert CL.percent_overshoot(y[:, None], [0.0], [1.0])[0] == pytest.approx(SECOND_ORDER_OVERSHOOT, rel=1e-5)
+
+
+def test_metrics_rise_time_ramp_and_zero_step():
+    t = np.linspace(0.0, 2.0, 201)
+    pos = np.minimum(t, 1.0)[:, None]
+    assert CL.rise_time(pos, [0.0], [1.0], rate=100.0)[0] == pytest.approx(0.9)
+    assert CL.rise_time(np.zeros((5, 1)), [0.0], [0.0], rate=100.0)[0] == 0.0
+    assert np.isnan(CL.rise_time(np.zeros((5, 1)), [0.0], [1.0], rate=100.0)[0])
+    assert np.isnan(CL.percent_overshoot(np.zeros((5, 1)), [0.0], [0.0])[0])
+
+
+def test_metrics_itae_exponential():
+    rate = 10000.0
+    t = np.arange(0, 5 * rate + 1) / rate
+    pos = (1 - np.exp(-t))[:, None]
+    assert CL.itae(pos, [1.0], rate)[0] == pytest.approx(EXP_ITAE, rel=1e-6)
+
+
+def test_actual_cost_pads_final_input():
+    X = np.array([[1.0, 0.0], [0.0, 0.0]])
+    U = np.array([[2.0]])
+    c = CL.actual_cost(X, U, np.eye(2), np.eye(1), np.zeros(2))
+    assert c == pytest.approx(1.0 + 4.0)
+    assert CL.cost_ratio(2.0, 0.0) != CL.cost_ratio(2.0, 0.0)  # NaN
+    assert CL.normalized_cost(3.0, 2.0) == 1.5
+
+
+def test_controller_validation_and_qp_kinds():
+    with pytest.raises(ValueError):
+        CL.Controller("pid")
+    with pytest.raises(ValueError):
+        CL.Controller("empc")
+    assert CL.Controller("empc", p=3).empc == P.EmpcSettings()
+    plant = D.Pendulum()
+    with pytest.raises(NotImplementedError):
+        CL.run_closed_loop(plant, CL.Controller("small"), _template(plant, 10, 5.0), np.zeros(2), np.zeros(2),
+                           0.05, 100.0)
+    with pytest.raises(ValueError):
+        CL.apply_error_multiplier(D.PendulumParams(), 0.0)
+    pp = CL.apply_error_multiplier(D.PendulumParams(), 1.3)
+    assert pp.mass == pytest.approx(1.3) and pp.length == pytest.approx(1.3)
+
+
+def test_pendulum_and_rk4():
+    plant = D.Pendulum(D.PendulumParams(gravity=0.0, damping=0.0))
+    x = D.integrate(plant.ode, np.array([0.0, 1.0]), np.array([0.0]), 0.5)
+    np.testing.assert_allclose(x, [0.5, 1.0], rtol=1e-12)  # free rotation
+    with pytest.raises(ValueError):
+        D.PendulumParams(mass=0.0)
+    # small-angle oscillation period of the undamped pendulum
+    plant = D.Pendulum(D.PendulumParams(damping=0.0))
+    x = np.array([1e-3, 0.0])
+    period = 2 * np.pi * np.sqrt(1.0 / 9.81)
+    for _ in range(100):
+        x = D.integrate(plant.ode, x, np.array([0.0]), period / 100)
+    np.testing.assert_allclose(x, [1e-3, 0.0], atol=1e-8)
+
+
+# ---------------------------------------------------------------------------
+# host loop with the oracle standing in for the device solve (CPU)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_host_loop_matches_reference_trace(name, monkeypatch):
+    g, plant, tpl, ctl = _case(name)
+
+    def oracle_solve(spec, sched, st, x0, prev=None, **_):
+        return O.solve_empc(O.Problem.from_spec(spec), sched.p, O.Settings.from_settings(st), x0, prev)
+
+    monkeypatch.setattr(CL, "solve_empc", oracle_solve)
+    res = CL.run_closed_loop(plant, ctl, tpl, np.zeros(plant.n), g["goal"], float(g["duration"]), 100.0)
+    np.testing.assert_allclose(res.inputs, g["inputs"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(res.states, g["states"], rtol=1e-9, atol=1e-9)
+
+
+# ---------------------------------------------------------------------------
+# CUDA path
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+def test_closed_loop_replay_matches_reference(name):
+    """FP64 device mode + the reference's draws: the whole closed-loop trace
+    (every period a warm solve on the device-resident population) equals the
+    reference's."""
+    g, plant, tpl, ctl = _case(name, precision="fp64")
+    fn = _replay(ctl.empc, ctl.p, tpl.u_min, tpl.u_max)
+    res = CL.run_closed_loop(plant, ctl, tpl, np.zeros(plant.n), g["goal"], float(g["duration"]), 100.0, _draws=fn)
+    np.testing.assert_allclose(res.inputs, g["inputs"], rtol=1e-7, atol=1e-8)
+    np.testing.assert_allclose(res.states, g["states"], rtol=1e-7, atol=1e-8)
+
+
+@pytest.mark.gpu
+def test_empc_controller_smoke():
+    """TST/test_closedloop.py:234-245 on the CUDA path with its own RNG."""
+    plant = D.Pendulum(D.PendulumParams(gravity=0.0))
+    tpl = _template(plant, 30, 25.0)
+    res = CL.run_closed_loop(plant, CL.Controller("empc", p=3, empc=P.EmpcSettings(num_sims=64, num_parents=8,
+                                                                                  generations=2)),
+                             tpl, x0=np.zeros(2), x_goal=np.array([0.4, 0.0]), duration=0.5, rate=100.0)
+    assert res.states.shape == (51, 2)
+    assert np.all(np.abs(res.inputs) <= 25.0 + 1e-9)
+    assert np.all(np.isfinite(res.states))
+    assert abs(res.states[-1, 0] - 0.4) < 0.1
+
+
+@pytest.mark.gpu
+def test_closed_loop_tracks_arm_goal():
+    plant = D.NLinkArm(D.NLinkParams(links=3))
+    tpl = _template(plant, 30, 2.0)
+    goal = np.array([0.3, -0.2, 0.1, 0, 0, 0])
+    res = CL.run_closed_loop(plant, CL.Controller("empc", p=4, empc=P.EmpcSettings(num_sims=1024, num_parents=64,
+                                                                                  generations=3, seed=1)),
+                             tpl, x0=np.zeros(6), x_goal=goal, duration=1.5, rate=100.0)
+    assert np.all(np.abs(res.inputs) <= 2.0 + 1e-9)
+    assert np.abs(res.states[-1, :3] - goal[:3]).max() < 0.05
+    rep = CL.compute_metrics(res, tpl.Q, tpl.R, goal, 100.0, 3)
+    assert rep.failures == 0 and np.isfinite(rep.actual_cost)
+
+
+@pytest.mark.gpu
+def test_fleet_steps_all_plants():
+    plants = [D.Pendulum(D.PendulumParams(gravity=0.0)) for _ in range(4)]
+    tpl = _template(plants[0], 30, 25.0)
+    goals = np.array([[0.4, 0.0], [-0.3, 0.0], [0.1, 0.0], [0.0, 0.0]])
+    fleet = CL.ClosedLoopFleet(plants, CL.Controller("empc", p=3, empc=P.EmpcSettings(num_sims=256, num_parents=16,
+                                                                                      generations=3)),
+                               tpl, goals, rate=100.0)
+    out = fleet.run(np.zeros((4, 2)), duration=0.8)
+    assert len(out) == 4
+    for r, g in zip(out, goals):
+        assert r.states.shape == (81, 2)
+        assert np.all(np.abs(r.inputs) <= 25.0 + 1e-9)
+        assert abs(r.states[-1, 0] - g[0]) < 0.05

@@ -9,5 +9,5 @@ timeout 1200 python bench.py --config c5 --steps 5 --warmup 3 --cpu-sample-s 10 
 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain_b.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_l.log 2>&1
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_b2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:rollout -s 20 -c 1 -o gpurun_out/prof_c3_rollout_bench python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_f.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"persist|rollout" -s 4 -c 1 -o gpurun_out/prof_c3_bench python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_f.log 2>&1
 tail -2 gpurun_out/ncu_f.log
