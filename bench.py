@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--variant", type=int, default=-1, help="force a rollout kernel variant")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scorer", default="rollout", choices=["rollout", "condensed"],
+                    help="rollout (the north-star kernels, default) or the reference's condensed quadratic "
+                         "(SURVEY §8 f2; FP64 quadratic form, roofline against the FP64 peak)")
     return ap.parse_args()
 
 
@@ -194,7 +197,7 @@ def run_population_sharded(args, rank, world):
 
     w = W.WORKLOADS[args.config]
     specs, x0s = W.build(w)
-    shard = PopulationShard(specs[0], w.schedule(), w.settings(), rank, world)
+    shard = PopulationShard(specs[0], w.schedule(), w.settings(scorer=args.scorer), rank, world)
     K, eb = shard.K, shard.entry_bytes
     gathered = torch.empty(world * K * eb, dtype=torch.uint8, device="cuda")
 
@@ -259,7 +262,7 @@ def run_ours(args):
         return run_population_sharded(args, rank, world)
     w_total, w, specs, x0s, scaling = workload(args, rank, world)
     sched = w.schedule()
-    st = w.settings()
+    st = w.settings(scorer=args.scorer)
     # --- device-resident path: the graph-captured cold solve
     if w.instances > 1:
         batch = P.EmpcBatch(specs, sched, st)
@@ -339,15 +342,24 @@ def run_ours(args):
     e2e_value = units_total / e2e_total
 
     # --- roofline of the dominant kernel (rollout: K2+K3 with the K5 prologue)
-    flop_per_launch = w.flop_per_candidate * w.scored_per_solve / max(nroll, 1)
+    condensed = args.scorer == "condensed"
+    if condensed:
+        # quadratic form z'Pz + 2g'z: 2 pm^2 + 4 pm FP64 flop per scored candidate
+        pm = w.p * w.m
+        flop_per_launch = (2 * pm * pm + 4 * pm) * w.scored_per_solve / max(nroll, 1)
+    else:
+        flop_per_launch = w.flop_per_candidate * w.scored_per_solve / max(nroll, 1)
     achieved = flop_per_launch / (rollout_ms * 1e-3) / 1e12
     peak, peak_src = 72.53, "tools/ffma_peak.cu on a B200 of this pool (no FP32 entry in MEASURED_PEAKS.json)"
     if os.path.exists(FP32_PEAK_FILE):
         with open(FP32_PEAK_FILE) as f:
             pk = json.load(f)
         peak, peak_src = pk["tflops"], pk.get("source", peak_src)
+        if condensed:
+            peak = pk.get("fp64_tflops", peak)
+            peak_src = pk.get("fp64_source", peak_src)
     traffic = None
-    if os.path.exists(TRAFFIC_FILE):
+    if os.path.exists(TRAFFIC_FILE) and not condensed:
         with open(TRAFFIC_FILE) as f:
             tr = json.load(f)
         traffic = tr.get(args.config)
@@ -355,16 +367,17 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (reference recipe: linearized N-link arms, SURVEY §8d)",
+        "dtype": "f32" if not condensed else "f32 population, f64 quadratic form", "scorer": args.scorer, "data": "synthetic (reference recipe: linearized N-link arms, SURVEY §8d)",
         "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}", "dof": w.dof, "T": w.T, "p": w.p,
                    "N": w.N, "K": w.K, "G": w.G, "instances": w_total.instances,
                    "instances_per_rank": w.instances, "l2": "flushed (256 MiB write) between timed solves",
                    "kernel_variant": ctx.h.describe()},
         "latency_ms": {"median": statistics.median(ms_each), "q1": float(np.percentile(ms_each, 25)),
                        "q3": float(np.percentile(ms_each, 75)), "min": min(ms_each)},
-        "roofline": {"bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "fp64_fma" if condensed else "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "persist_kernel (whole solve in one cooperative launch: rollouts + selection)"
+                     "kernel": "cond_score_kernel (breed + FP64 quadratic form)" if condensed else
+                     "persist_kernel (whole solve in one cooperative launch: rollouts + selection)"
                      if "persistent" in ctx.h.describe() else "rollout_kernel",
                      "rollout_ms_per_launch": rollout_ms, "rollout_launches_per_step": nroll,
                      "flop_per_launch": flop_per_launch, "peak_source": peak_src},

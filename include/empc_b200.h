@@ -14,6 +14,10 @@
  *   empc_select   <- argsort(kind="stable")[:K] / argmin   empc.py:185-186, 234
  *   empc_expand   <- expand / input_at   param.py:91-116   (knots -> inputs)
  *   empc_set_schedule <- KnotSchedule.coeffs / interpolation_matrix param.py:49-111
+ *   empc_set_scorer   <- _CostModel's choice of scorer     empc.py:133-152 (rollout vs
+ *                        condensed quadratic from build_small_param, condense.py:268-274)
+ *   empc_set_scorer   <- _CostModel's choice of scorer     empc.py:133-152 (rollout vs
+ *                        condensed quadratic from build_small_param, condense.py:268-274)
  *   empc_set_problems <- MpcSpec + DiscreteLinearModel condense.py:42-87, dynamics.py:223-238
  *
  * Conventions: row-major arrays; every pointer argument is a HOST pointer
@@ -68,6 +72,26 @@ const char* empc_last_error(const empc_handle* h);
 /* Knot schedule: per step k in [0,T): u_k = (1-c_k) U[idx1_k] + c_k U[idx2_k]
  * (param.py:30-46, p==1 -> idx1=idx2=0, c=0). */
 int empc_set_schedule(empc_handle* h, const int32_t* idx1, const int32_t* idx2, const double* c);
+
+/* Scorer of every subsequent run / score call:
+ *   EMPC_SCORER_ROLLOUT   (0, default) FP32/FP64 horizon rollout (empc.py:85-119)
+ *   EMPC_SCORER_CONDENSED (1) the reference's own condensed quadratic
+ *     J(z) = z'Pz + 2q'z + c0 (empc.py:133-152), built on the device once per
+ *     run in FP64 and evaluated in FP64 (costs rounded to the population
+ *     precision).  Not for state-bounded specs (the reference rolls those out). */
+#define EMPC_SCORER_ROLLOUT 0
+#define EMPC_SCORER_CONDENSED 1
+int empc_set_scorer(empc_handle* h, int32_t scorer);
+
+/* Scorer of every subsequent run / score call:
+ *   EMPC_SCORER_ROLLOUT   (0, default) FP32/FP64 horizon rollout (empc.py:85-119)
+ *   EMPC_SCORER_CONDENSED (1) the reference's own condensed quadratic
+ *     J(z) = z'Pz + 2q'z + c0 (empc.py:133-152), built on the device once per
+ *     run in FP64 and evaluated in FP64 (costs rounded to the population
+ *     precision).  Not for state-bounded specs (the reference rolls those out). */
+#define EMPC_SCORER_ROLLOUT 0
+#define EMPC_SCORER_CONDENSED 1
+int empc_set_scorer(empc_handle* h, int32_t scorer);
 
 /* Problems of instances [first, first+count).  Per instance, contiguous:
  * Ad[n*n] Bd[n*m] wd[n] Q[n*n] R[m*m] x_goal[n] u_goal[m] u_min[m] u_max[m]. */

@@ -21,7 +21,7 @@ EMPC_FP32, EMPC_FP64 = 0, 1
 
 # every symbol include/empc_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_problems",
+    "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_scorer", "empc_set_problems",
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
     "empc_set_variant", "empc_set_occupancy", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
@@ -86,6 +86,7 @@ def load(path: str | None = None):
         "empc_destroy": (None, [P]),
         "empc_last_error": (C.c_char_p, [P]),
         "empc_set_schedule": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), D]),
+        "empc_set_scorer": (C.c_int, [P, C.c_int32]),
         "empc_set_problems": (C.c_int, [P, I32, I32] + [D] * 9),
         "empc_pop_alloc": (C.c_int, [P, C.POINTER(I32)]),
         "empc_pop_free": (C.c_int, [P, I32]),

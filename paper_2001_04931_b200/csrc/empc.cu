@@ -21,6 +21,7 @@
 #include "../../include/empc_b200.h"
 #define EMPC_HOST_TU
 #include "empc_kernels.cuh"
+#include "empc_cond.h"
 #include "empc_variants.h"
 
 using namespace empc;
@@ -65,6 +66,7 @@ class EngineBase {
   virtual ~EngineBase() = default;
   std::string err;
   virtual void set_schedule(const int32_t*, const int32_t*, const double*) = 0;
+  virtual void set_scorer(int) = 0;
   virtual void set_problems(int, int, const double* const*) = 0;
   virtual int pop_alloc() = 0;
   virtual void pop_free(int) = 0;
@@ -152,11 +154,17 @@ class Engine final : public EngineBase {
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
     CK(cudaMalloc(&cw_, sizeof(S) * d_.T));
     CK(cudaMalloc(&G_, sizeof(S) * d_.p * d_.p));
+    CK(cudaMalloc(&W64_, sizeof(double) * d_.T * d_.p));
+    CK(cudaMalloc(&G64_, sizeof(double) * d_.p * d_.p));
+    ck_ = cond_kernels<S>();
     select_smem_ = select_smem<S>(d_.N);
     if (select_smem_ > (size_t)kMaxSmem - 1024) throw InvalidArg{"num_sims too large for the selection kernel"};
     // function attributes are process-wide: always the maximum, never a per-engine size
     CK(cudaFuncSetAttribute(select_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
     for (auto& v : variants_) CK(cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CK(cudaFuncSetAttribute(ck_.score_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CK(cudaFuncSetAttribute(ck_.score_glob, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CK(cudaFuncSetAttribute(ck_.prep, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
   }
 
   ~Engine() override {
@@ -168,6 +176,9 @@ class Engine final : public EngineBase {
     for (int b = 0; b < 2; ++b) { cudaFree(pop_[b]); cudaFree(cost_[b]); }
     cudaFree(elite_); cudaFree(qcount_); cudaFree(qlist_); cudaFree(out_d_); cudaFreeHost(out_h_);
     cudaFree(idx1_); cudaFree(idx2_); cudaFree(cw_); cudaFree(G_);
+    cudaFree(W64_); cudaFree(G64_);
+    if (cond_) cudaFree(cond_);
+    if (cws_) cudaFree(cws_);
     if (scratch_pop_) cudaFree(scratch_pop_);
     if (scratch_cost_) cudaFree(scratch_cost_);
     if (scratch_dbl_) cudaFree(scratch_dbl_);
@@ -190,17 +201,111 @@ class Engine final : public EngineBase {
       if (c[k] > 0.0) Wd[(size_t)k * p + i2[k]] += c[k];
     }
     std::vector<S> G((size_t)p * p);
+    std::vector<double> G64((size_t)p * p);
     for (int a = 0; a < p; ++a)
       for (int b = 0; b < p; ++b) {
         double s = 0.0;
         for (int k = 0; k < T; ++k) s += Wd[(size_t)k * p + a] * Wd[(size_t)k * p + b];
         G[(size_t)a * p + b] = (S)s;
+        G64[(size_t)a * p + b] = s;
       }
+    CK(cudaMemcpy(W64_, Wd.data(), sizeof(double) * T * p, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(G64_, G64.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(idx1_, i1, sizeof(int) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(idx2_, i2, sizeof(int) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(cw_, cs.data(), sizeof(S) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(G_, G.data(), sizeof(S) * p * p, cudaMemcpyHostToDevice));
     have_sched_ = true;
+  }
+
+  // -- scorer: 0 = rollout (K/empc.py:85-119), 1 = condensed quadratic (K/empc.py:122-152)
+  void set_scorer(int sc) override {
+    if (sc != 0 && sc != 1) throw InvalidArg{"scorer must be 0 (rollout) or 1 (condensed)"};
+    scorer_ = sc;
+  }
+
+  // Device build of the condensed model for every instance (empc_cond.h):
+  // sensitivities + u_goal trajectory, split-K Gram of [P | g], reduction.
+  // Instances are processed in chunks that keep the workspace <= 256 MiB.
+  void launch_cond_build() {
+    const int n = d_.n, m = d_.m, T = d_.T, p = d_.p, pm = d_.pm;
+    ensure_cond_ws();
+    const int ksp = n >= 16 ? 4 : (n >= 4 ? 2 : 1);
+    const int cbmax = std::max(1, std::min(pm, 1024 / (n * ksp)));
+    int cb = std::max(1, std::min(cbmax, (pm * I_ + sms_ - 1) / sms_));
+    const int chunks = (pm + cb - 1) / cb;
+    cb = (pm + chunks - 1) / chunks;
+    const int threads = std::max(64, std::min(1024, (n * cb * ksp + 31) / 32 * 32));
+    const size_t psm = cond_prep_smem(n, cb, dense_ ? 1 : 0);
+    if (psm > (size_t)kMaxSmem) throw InvalidArg{"condensed scorer: state dimension too large for the build kernel"};
+    const int K = T * n;
+    const int ntc = (pm + 1 + kCondTile - 1) / kCondTile;
+    const int tiles = ntc * (ntc + 1) / 2;
+    const size_t fixed = (size_t)K * pm * (dense_ ? 2 : 1) + K + 1;
+    // split-K depends on the shape only: P has the same bits for batched,
+    // sharded and single runs
+    const int splits = std::max(1, (K + 255) / 256);
+    const size_t per = fixed + (size_t)splits * pm * (pm + 1);
+    const int ic = (int)std::max<size_t>(1, std::min<size_t>(I_, ((size_t)256 << 20) / sizeof(double) / per));
+    if (per * ic > cws_n_) throw CudaError{"condensed workspace not allocated"};
+    CondBuild b{};
+    b.n = n; b.m = m; b.T = T; b.p = p; b.pm = pm;
+    b.SL = SL_; b.prob = stage_prob_d_; b.state = stage_state_d_;
+    b.W = W64_; b.G = G64_;
+    b.S = cws_;
+    b.QS = dense_ ? cws_ + (size_t)ic * K * pm : nullptr;
+    b.E = cws_ + (size_t)ic * K * pm * (dense_ ? 2 : 1);
+    b.part = b.E + (size_t)ic * (K + 1);
+    b.cond = cond_;
+    b.cb = cb; b.ksp = ksp; b.splits = splits; b.dense = dense_ ? 1 : 0;
+    for (int i0 = 0; i0 < I_; i0 += ic) {
+      const int cnt = std::min(ic, I_ - i0);
+      b.inst0 = i0;
+      launch_ex(ck_.prep, dim3(chunks + 1, cnt), dim3(threads), psm, false, b);
+      launch_ex(ck_.gram, dim3(tiles, splits, cnt), dim3(256), 0, false, b);
+      launch_ex(ck_.finish, dim3((pm * pm + pm + 1 + 255) / 256, cnt), dim3(256), 0, false, b);
+      launches_ += 3;
+    }
+    pdl_next_ = use_pdl_;
+  }
+
+  // workspace of launch_cond_build (allocated outside graph capture)
+  void ensure_cond_ws() {
+    const int n = d_.n, T = d_.T, pm = d_.pm;
+    if (!cond_) CK(cudaMalloc(&cond_, sizeof(double) * (size_t)I_ * cond_layout(pm).stride));
+    const int K = T * n;
+    const int splits = std::max(1, (K + 255) / 256);
+    const size_t per = (size_t)K * pm * (dense_ ? 2 : 1) + K + 1 + (size_t)splits * pm * (pm + 1);
+    const int ic = (int)std::max<size_t>(1, std::min<size_t>(I_, ((size_t)256 << 20) / sizeof(double) / per));
+    if (per * ic > cws_n_) {
+      if (cws_) cudaFree(cws_);
+      CK(cudaMalloc(&cws_, sizeof(double) * per * ic));
+      cws_n_ = per * ic;
+    }
+  }
+
+  struct CondPlan {
+    int tile, tileP, tiles, threads, tPS;
+    size_t smem;
+    bool psm;
+  };
+  CondPlan plan_cond(int nc) const {
+    CondPlan c{};
+    int tile = I_ == 1 ? (nc + sms_ - 1) / sms_ : kCondMaxTile;
+    tile = std::max(1, std::min({tile, kCondMaxTile, std::max(nc, 1)}));
+    c.tiles = std::max(1, (nc + tile - 1) / tile);
+    c.tile = std::max(1, (nc + c.tiles - 1) / c.tiles);
+    c.tileP = (c.tile + kCondCC - 1) / kCondCC * kCondCC;
+    const int ncg = c.tileP / kCondCC;
+    const int pmS = (d_.pm + kCondRB - 1) / kCondRB * kCondRB;
+    c.threads = std::max(64, std::min(512, (ncg * (pmS / kCondRB) + 31) / 32 * 32));
+    CondSmem s = cond_smem<S>(d_.pm, d_.m, c.tileP, c.threads, true);
+    c.psm = s.total <= (size_t)kMaxSmem;
+    if (!c.psm) s = cond_smem<S>(d_.pm, d_.m, c.tileP, c.threads, false);
+    if (s.total > (size_t)kMaxSmem) throw InvalidArg{"condensed scorer: knot vector too long"};
+    c.smem = s.total;
+    c.tPS = s.tPS;
+    return c;
   }
 
   // -- problems (FP64 host -> pinned staging; uploaded inside the run) --------
@@ -371,14 +476,28 @@ class Engine final : public EngineBase {
   void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,
                       const int* inj_par = nullptr, const uint8_t* inj_take = nullptr, const uint8_t* inj_mut = nullptr,
                       const double* inj_noise = nullptr, const S* inj_init = nullptr) {
-    const Variant<S>& v = pick();
-    const Launch L = plan(v, nc);
+    Launch L{};
+    void (*kern)(RolloutArgs<S>) = nullptr;
+    int tPS = 0;
+    if (scorer_ == 1) {
+      const CondPlan c = plan_cond(nc);
+      L.tile = c.tile; L.tileP = c.tileP; L.tiles = c.tiles; L.threads = c.threads; L.smem = c.smem;
+      tPS = c.tPS;
+      kern = c.psm ? ck_.score_smem : ck_.score_glob;
+    } else {
+      const Variant<S>& v = pick();
+      L = plan(v, nc);
+      tPS = tps_for(L.tileP);
+      kern = v.kernel;
+    }
     RolloutArgs<S> a{};
     a.d = d_; a.SL = SL_; a.mode = mode; a.r_diag = r_diag_ ? 1 : 0;
     a.nc = nc; a.row0 = row0; a.rows = rows;
-    a.tile = L.tile; a.tileP = L.tileP; a.tPS = tps_for(L.tileP); a.evolve = evolve;
+    a.tile = L.tile; a.tileP = L.tileP; a.tPS = tPS; a.evolve = evolve;
     a.cand_base = cand_base_;
     a.copy_elites = elites_copied_ ? 0 : 1;
+    a.cond = cond_;
+    a.cstride = cond_layout(d_.pm).stride;
     elites_copied_ = false;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
@@ -394,7 +513,7 @@ class Engine final : public EngineBase {
       a.dbg = dbg_;
       dbg_ctas_ = (int)(L.tiles * I_);
     }
-    launch_ex(v.kernel, dim3(L.tiles, I_), dim3(L.threads), L.smem, pdl_next_, a);
+    launch_ex(kern, dim3(L.tiles, I_), dim3(L.threads), L.smem, pdl_next_, a);
     pdl_next_ = use_pdl_;
     ++launches_;
     ++rollout_launches_;
@@ -443,7 +562,7 @@ class Engine final : public EngineBase {
   // configuration does not qualify and the per-generation launches are used.
   template <typename Pre, typename Post>
   bool try_persistent(const empc_run_args& r, bool timed, Pre& pre, Post& post) {
-    if (!persist_enabled_ || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K)
+    if (!persist_enabled_ || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K)
       return false;
     const Variant<S>& v = pick();
     const PersistVariant<S>* pv = nullptr;
@@ -529,6 +648,7 @@ class Engine final : public EngineBase {
     int cur = 0;
     const size_t pm = d_.pm;
     if (inj == nullptr && try_persistent(r, timed_rollouts, pre, post)) return r.evolves & 1;
+    if (scorer_ == 1 && (r.init || r.rescore || r.evolves > 0)) launch_cond_build();
     if (r.init) {
       const S* inj_init = inj ? (const S*)(*inj)[0] : nullptr;
       pre();
@@ -600,9 +720,10 @@ class Engine final : public EngineBase {
   }
 
   cudaGraphExec_t graph_for(const empc_run_args& r) {
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_);
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;
+    if (scorer_ == 1) ensure_cond_ws();
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     int cur = 0;
@@ -661,7 +782,7 @@ class Engine final : public EngineBase {
         if (p) cudaFree(p);
     } else {
       cudaGraphExec_t ge = graph_for(r);
-      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_)];
+      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_)];
       CK(cudaGraphLaunch(ge, stream_));
     }
     if (r.slot_out >= 0) {
@@ -696,6 +817,7 @@ class Engine final : public EngineBase {
     ensure_scratch((size_t)I_ * num);
     upload_cast(cands, scratch_pop_, nc);
     pdl_next_ = false;
+    if (scorer_ == 1) launch_cond_build();
     launch_rollout(kScore, num, 0, num, 0, scratch_pop_, nullptr, scratch_pop_, scratch_cost_);
     pdl_next_ = false;
     download_uncast(scratch_cost_, costs, (size_t)I_ * num);
@@ -734,7 +856,7 @@ class Engine final : public EngineBase {
                    int32_t* nlaunch) override {
     stage_run(r);
     cudaGraphExec_t ge = graph_for(r);
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_);
+    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_);
     if (flush && !flush_) {
       flush_n_ = (size_t)256 << 20 >> 4;  // 256 MiB > 126 MB L2
       CK(cudaMalloc(&flush_, flush_n_ * 16));
@@ -814,6 +936,7 @@ class Engine final : public EngineBase {
     rr.slot_in = -1;
     stage_run(rr);
     pdl_next_ = false;
+    if (scorer_ == 1) launch_cond_build();
     cand_base_ = (int)sh_init_base_;
     launch_rollout(kInitPhilox, sh_init_, d_.K, d_.N, 0, nullptr, nullptr, pop_[0], cost_[0]);
     cand_base_ = 0;
@@ -861,6 +984,7 @@ class Engine final : public EngineBase {
     rr.init = 1;  // staging only: the population stays where it is
     stage_run(rr);
     pdl_next_ = false;
+    if (scorer_ == 1) launch_cond_build();
     cand_base_ = (int)sh_child_base_;
     int* saved_q = qcount_;
     qcount_ = nullptr;
@@ -893,6 +1017,13 @@ class Engine final : public EngineBase {
   }
 
   std::string describe() override {
+    if (scorer_ == 1) {
+      const CondPlan c = plan_cond(d_.N - d_.K);
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "condensed scorer (FP64 quadratic form) | evolve tile=%d tiles=%d threads=%d smem=%zu P_in_smem=%d | sms=%d",
+                    c.tile, c.tiles, c.threads, c.smem, (int)c.psm, sms_);
+      return buf;
+    }
     const Variant<S>& v = pick();
     const Launch a = plan(v, d_.N - d_.K);
     char buf[512];
@@ -985,6 +1116,12 @@ class Engine final : public EngineBase {
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr;
   S *cw_ = nullptr, *G_ = nullptr;
+  double *W64_ = nullptr, *G64_ = nullptr;  // FP64 W (T x p) and W'W for the condensed build
+  int scorer_ = 0;
+  CondKernels<S> ck_{};
+  double* cond_ = nullptr;  // per instance: P, g, ref, J_ref
+  double* cws_ = nullptr;   // build workspace
+  size_t cws_n_ = 0;
   size_t select_smem_ = 0;
   bool have_sched_ = false, have_prob_ = false, r_diag_ = true;
   std::vector<Slot> slots_;
@@ -994,7 +1131,7 @@ class Engine final : public EngineBase {
   uint4* flush_ = nullptr;
   size_t flush_n_ = 0;
   std::vector<cudaEvent_t> ev_;
-  using GKey = std::tuple<bool, bool, int, int, bool, int>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int>;
   std::map<GKey, cudaGraphExec_t> graphs_;
   std::map<GKey, int> graph_cur_, graph_launches_, graph_rollouts_;
   int launches_ = 0, rollout_launches_ = 0;
@@ -1062,6 +1199,10 @@ void empc_destroy(empc_handle* h) { delete h; }
 const char* empc_last_error(const empc_handle* h) {
   if (!h || !h->eng) return g_create_error.c_str();
   return h->eng->err.c_str();
+}
+
+int empc_set_scorer(empc_handle* h, int32_t scorer) {
+  GUARD(h, { h->eng->set_scorer(scorer); });
 }
 
 int empc_set_schedule(empc_handle* h, const int32_t* idx1, const int32_t* idx2, const double* c) {

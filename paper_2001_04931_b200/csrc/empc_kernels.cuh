@@ -75,6 +75,8 @@ struct RolloutArgs {
   int* qcount;              // per instance: children that beat the K-th elite (incremental selection)
   void* qlist;              // per instance: [qcap] (ord key, row) pairs
   int qcap;
+  const double* cond;       // condensed scorer: per instance P, g, ref, J_ref (empc_cond.h)
+  int cstride;              // doubles per instance of `cond`
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -134,6 +136,158 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
+// K5 prologue shared by the rollout and the condensed scorer: random draws
+// (phase 1a, independent of the producer grid), then -- after the PDL wait --
+// the elite carry-over and the tile's candidate knots into UsT[gene][cand]
+// (phase 1b).  Returns false when the CTA has no candidates.
+template <typename S>
+__device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, int tile0, int cnt, int tileP, int tPS,
+                                           S* UsT, int* src, uint32_t* tbits, const S* cumin, const S* cumax,
+                                           const S* csig, size_t pop_base) {
+  const Dims& d = a.d;
+  const int m = d.m, pm = d.pm;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const double* __restrict__ X = a.state + (size_t)inst * a.SL.sstride;
+  const StageLayout& SL = a.SL;
+  const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
+  // ---- phase 1a: random draws -- counter-based, so also independent of the
+  // producer grid (the run parameters are staged by the host copy)
+  const RunParams rp = *a.run;
+  const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
+  const uint32_t gen = (uint32_t)(rp.gen0 + a.evolve);
+  const bool philox_breed = a.mode == kBreedPhilox;
+  if (cnt > 0) {
+    if (breed) {
+      // parents (K/empc.py:196): two uniform elite ranks per child
+      for (int c = tid; c < cnt; c += nthr) {
+        const int child = tile0 + c;
+        const uint32_t gchild = (uint32_t)(a.cand_base + child);
+        if (a.mode == kBreedInject) {
+          const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
+          src[2 * c] = pp[0];
+          src[2 * c + 1] = pp[1];
+        } else {
+          const U4 r = philox4x32_10(U4{kParentWord, gchild, (uint32_t)inst, gen}, key0, key1);
+          src[2 * c] = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
+          src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)d.K);
+        }
+      }
+    }
+    if (philox_breed || a.mode == kInitPhilox) {
+      // crossover bit + mutation offset (K/empc.py:197-199), or the uniform
+      // initial knot (K/empc.py:170), per gene into UsT; unrolled so several
+      // independent Philox chains are in flight per thread
+#pragma unroll 4
+      for (int e0 = 0; e0 < tileP * pm; e0 += nthr) {
+        const int e = e0 + tid;
+        const int c = e / pm, g = e - (e / pm) * pm;
+        bool take = false;
+        if (e < tileP * pm && c < cnt) {
+          const int l = g % m;
+          const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
+          if (philox_breed) {
+            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, gen}, key0, key1);
+            take = (uint64_t)r.x < rp.thr_cross;
+            const bool mut = (uint64_t)r.y < rp.thr_mut;
+            UsT[g * tPS + c] = mut ? normal_bm<S>(r.z, r.w) * csig[l] : S(0);
+          } else {
+            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, kInitTag}, key0, key1);
+            const S lo = cumin[l], hi = cumax[l];
+            const S v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
+            UsT[g * tPS + c] = v > hi ? hi : v;
+          }
+        }
+        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, take);
+        if (lane == 0 && e0 + warp * 32 < tileP * pm) tbits[(e0 + warp * 32) >> 5] = bits;
+      }
+    }
+  }
+
+  EMPC_MARK(1)
+  // ---- phase 1b: everything below reads the producer grid's outputs
+  pdl_wait();
+  EMPC_MARK(2)
+  // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
+  // population are the sorted elites with their carried costs.
+  if (breed && a.copy_elites) {  // otherwise the selection kernel already did
+    for (int e = blockIdx.x; e < d.K; e += gridDim.x) {
+      const int s = a.elite_idx[(size_t)inst * d.K + e];
+      const S* from = a.pop_in + (pop_base + s) * pm;
+      S* to = a.pop_out + (pop_base + e) * pm;
+      for (int g = tid; g < pm; g += nthr) to[g] = from[g];
+      if (tid == 0) a.cost_out[pop_base + e] = a.cost_in[pop_base + s];
+    }
+  }
+  if (cnt <= 0) return false;
+  EMPC_MARK(9)
+  if (breed) {
+    for (int c = tid; c < cnt; c += nthr) {  // elite ranks -> population rows
+      src[2 * c] = a.elite_idx[(size_t)inst * d.K + src[2 * c]];
+      src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + src[2 * c + 1]];
+    }
+  }
+  __syncthreads();  // src, phase-0/1a smem
+  EMPC_MARK(10)
+  // candidate knots -> UsT[gene][cand] (+ the population rows)
+  if (philox_breed) {
+    // crossover, mutation, clip (K/empc.py:201-204): a tight loop so the
+    // parent gathers of several genes are in flight together
+#pragma unroll 8
+    for (int e = tid; e < cnt * pm; e += nthr) {
+      const int c = e / pm, g = e - (e / pm) * pm;
+      const int l = g % m;
+      const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
+      const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+      const S lo = cumin[l], hi = cumax[l];
+      S v = par + UsT[g * tPS + c];
+      v = v < lo ? lo : (v > hi ? hi : v);
+      a.pop_out[(pop_base + a.row0 + tile0 + c) * pm + g] = v;
+      UsT[g * tPS + c] = v;
+    }
+    for (int e = cnt * pm + tid; e < tileP * pm; e += nthr) {
+      const int c = e / pm, g = e - (e / pm) * pm;
+      UsT[g * tPS + c] = S(0);
+    }
+  } else
+#pragma unroll 4
+  for (int e = tid; e < tileP * pm; e += nthr) {
+    const int c = e / pm, g = e - (e / pm) * pm;
+    S v = S(0);
+    if (c < cnt) {
+      const int l = g % m;
+      const int cand = tile0 + c;
+      if (a.mode == kScore) {
+        v = a.pop_in[(pop_base + a.row0 + cand) * pm + g];
+      } else if (a.mode == kInitPhilox) {
+        v = UsT[g * tPS + c];
+      } else if (a.mode == kInitInject) {
+        v = a.inj_init[((size_t)inst * a.nc + cand) * pm + g];
+      } else if (philox_breed) {
+        // crossover, mutation, clip (K/empc.py:201-204)
+        const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
+        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+        const S lo = cumin[l], hi = cumax[l];
+        v = par + UsT[g * tPS + c];
+        v = v < lo ? lo : (v > hi ? hi : v);
+      } else {
+        // injected draws, with the reference's FP64 arithmetic child + mutate*noise*sigma
+        const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
+        const bool take = a.inj_take[gi] != 0, mut = a.inj_mut[gi] != 0;
+        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+        const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
+        v = (S)((double)par + nz);
+        const S lo = cumin[l], hi = cumax[l];
+        v = v < lo ? lo : (v > hi ? hi : v);
+      }
+      if (a.mode != kScore) a.pop_out[(pop_base + a.row0 + cand) * pm + g] = v;
+    }
+    UsT[g * tPS + c] = v;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // rollout: K2 + K3 with the K5 breed / init prologue.
 //
 // Thread (rg, cg) owns rows {rg + r*NRG} (r < RR) of candidates
@@ -161,7 +315,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Dims& d = a.d;
   const StageLayout& SL = a.SL;
-  const int n = d.n, m = d.m, T = d.T, p = d.p, pm = d.pm;
+  const int n = d.n, m = d.m, T = d.T, p = d.p;
   const int tileP = a.tileP, tPS = a.tPS;
   const int inst = blockIdx.y;
   const int tile0 = blockIdx.x * a.tile;
@@ -182,7 +336,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   int* sI2 = sI1 + T;
   S* sC = reinterpret_cast<S*>(sI2 + T); ptr += sp.sched;
   S* sG = reinterpret_cast<S*>(ptr); ptr += sp.g;     // [p*p] + cost0
-  S* cU = reinterpret_cast<S*>(ptr); ptr += sp.cu;
+  ptr += sp.cu;  // per-candidate scratch slot of the plan (unused by this variant family)
   int* src = reinterpret_cast<int*>(ptr); ptr += sp.src;
   S* cw_ = reinterpret_cast<S*>(ptr); ptr += sp.cv;   // w, qd, xg, x0 [NP]; ug, umin, umax, sig, rdiag [m]
   S* cqd = cw_ + NP;
@@ -266,140 +420,8 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     if (lane == 0) cw_[i] += acc;
   }
   EMPC_MARK(8)
-  // ---- phase 1a: random draws -- counter-based, so also independent of the
-  // producer grid (the run parameters are staged by the host copy)
-  const RunParams rp = *a.run;
-  const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
-  const uint32_t gen = (uint32_t)(rp.gen0 + a.evolve);
   uint32_t* tbits = reinterpret_cast<uint32_t*>(cw_ + 4 * NP + 5 * m);  // crossover bits, 1 per gene
-  const bool philox_breed = a.mode == kBreedPhilox;
-  if (cnt > 0) {
-    if (breed) {
-      // parents (K/empc.py:196): two uniform elite ranks per child
-      for (int c = tid; c < cnt; c += nthr) {
-        const int child = tile0 + c;
-        const uint32_t gchild = (uint32_t)(a.cand_base + child);
-        if (a.mode == kBreedInject) {
-          const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
-          src[2 * c] = pp[0];
-          src[2 * c + 1] = pp[1];
-        } else {
-          const U4 r = philox4x32_10(U4{kParentWord, gchild, (uint32_t)inst, gen}, key0, key1);
-          src[2 * c] = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
-          src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)d.K);
-        }
-      }
-    }
-    if (philox_breed || a.mode == kInitPhilox) {
-      // crossover bit + mutation offset (K/empc.py:197-199), or the uniform
-      // initial knot (K/empc.py:170), per gene into UsT; unrolled so several
-      // independent Philox chains are in flight per thread
-#pragma unroll 4
-      for (int e0 = 0; e0 < tileP * pm; e0 += nthr) {
-        const int e = e0 + tid;
-        const int c = e / pm, g = e - (e / pm) * pm;
-        bool take = false;
-        if (e < tileP * pm && c < cnt) {
-          const int l = g % m;
-          const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
-          if (philox_breed) {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, gen}, key0, key1);
-            take = (uint64_t)r.x < rp.thr_cross;
-            const bool mut = (uint64_t)r.y < rp.thr_mut;
-            UsT[g * tPS + c] = mut ? normal_bm<S>(r.z, r.w) * csig[l] : S(0);
-          } else {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, kInitTag}, key0, key1);
-            const S lo = cumin[l], hi = cumax[l];
-            const S v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
-            UsT[g * tPS + c] = v > hi ? hi : v;
-          }
-        }
-        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, take);
-        if (lane == 0 && e0 + warp * 32 < tileP * pm) tbits[(e0 + warp * 32) >> 5] = bits;
-      }
-    }
-  }
-
-  EMPC_MARK(1)
-  // ---- phase 1b: everything below reads the producer grid's outputs
-  pdl_wait();
-  EMPC_MARK(2)
-  // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
-  // population are the sorted elites with their carried costs.
-  if (breed && a.copy_elites) {  // otherwise the selection kernel already did
-    for (int e = blockIdx.x; e < d.K; e += gridDim.x) {
-      const int s = a.elite_idx[(size_t)inst * d.K + e];
-      const S* from = a.pop_in + (pop_base + s) * pm;
-      S* to = a.pop_out + (pop_base + e) * pm;
-      for (int g = tid; g < pm; g += nthr) to[g] = from[g];
-      if (tid == 0) a.cost_out[pop_base + e] = a.cost_in[pop_base + s];
-    }
-  }
-  if (cnt <= 0) return;
-  EMPC_MARK(9)
-  if (breed) {
-    for (int c = tid; c < cnt; c += nthr) {  // elite ranks -> population rows
-      src[2 * c] = a.elite_idx[(size_t)inst * d.K + src[2 * c]];
-      src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + src[2 * c + 1]];
-    }
-  }
-  __syncthreads();  // src, phase-0/1a smem
-  EMPC_MARK(10)
-  // candidate knots -> UsT[gene][cand] (+ the population rows)
-  if (philox_breed) {
-    // crossover, mutation, clip (K/empc.py:201-204): a tight loop so the
-    // parent gathers of several genes are in flight together
-#pragma unroll 8
-    for (int e = tid; e < cnt * pm; e += nthr) {
-      const int c = e / pm, g = e - (e / pm) * pm;
-      const int l = g % m;
-      const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
-      const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
-      const S lo = cumin[l], hi = cumax[l];
-      S v = par + UsT[g * tPS + c];
-      v = v < lo ? lo : (v > hi ? hi : v);
-      a.pop_out[(pop_base + a.row0 + tile0 + c) * pm + g] = v;
-      UsT[g * tPS + c] = v;
-    }
-    for (int e = cnt * pm + tid; e < tileP * pm; e += nthr) {
-      const int c = e / pm, g = e - (e / pm) * pm;
-      UsT[g * tPS + c] = S(0);
-    }
-  } else
-#pragma unroll 4
-  for (int e = tid; e < tileP * pm; e += nthr) {
-    const int c = e / pm, g = e - (e / pm) * pm;
-    S v = S(0);
-    if (c < cnt) {
-      const int l = g % m;
-      const int cand = tile0 + c;
-      if (a.mode == kScore) {
-        v = a.pop_in[(pop_base + a.row0 + cand) * pm + g];
-      } else if (a.mode == kInitPhilox) {
-        v = UsT[g * tPS + c];
-      } else if (a.mode == kInitInject) {
-        v = a.inj_init[((size_t)inst * a.nc + cand) * pm + g];
-      } else if (philox_breed) {
-        // crossover, mutation, clip (K/empc.py:201-204)
-        const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
-        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
-        const S lo = cumin[l], hi = cumax[l];
-        v = par + UsT[g * tPS + c];
-        v = v < lo ? lo : (v > hi ? hi : v);
-      } else {
-        // injected draws, with the reference's FP64 arithmetic child + mutate*noise*sigma
-        const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
-        const bool take = a.inj_take[gi] != 0, mut = a.inj_mut[gi] != 0;
-        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
-        const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
-        v = (S)((double)par + nz);
-        const S lo = cumin[l], hi = cumax[l];
-        v = v < lo ? lo : (v > hi ? hi : v);
-      }
-      if (a.mode != kScore) a.pop_out[(pop_base + a.row0 + cand) * pm + g] = v;
-    }
-    UsT[g * tPS + c] = v;
-  }
+  if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
   __syncthreads();
   EMPC_MARK(3)
 

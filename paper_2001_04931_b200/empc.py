@@ -36,8 +36,11 @@ from .param import KnotSchedule, schedule_arrays
 class EmpcSettings:
     """Population shape and variation operators (K/empc.py:27-48).
 
-    ``precision`` is an extension: "fp32" (default) or "fp64" device
-    arithmetic.
+    Extensions: ``precision`` "fp32" (default) or "fp64" device arithmetic;
+    ``scorer`` "rollout" (default: the horizon rollout, K/empc.py:85-119) or
+    "condensed" (the reference's own knot-space quadratic, K/empc.py:122-152,
+    built on the device once per solve and evaluated in FP64).  State-bounded
+    specs always roll out, as in the reference (K/empc.py:138).
     """
 
     num_sims: int = 1024
@@ -50,6 +53,7 @@ class EmpcSettings:
     dist_ref: float = 1.0
     seed: int = 0
     precision: str = "fp32"
+    scorer: str = "rollout"
 
     def __post_init__(self):
         if self.num_sims < 1 or not 1 <= self.num_parents <= self.num_sims:
@@ -61,6 +65,8 @@ class EmpcSettings:
                 raise ValueError(f"{name} must lie in [0, 1]")
         if self.precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
+        if self.scorer not in ("rollout", "condensed"):
+            raise ValueError("scorer must be 'rollout' or 'condensed'")
 
 
 class Population:
@@ -212,12 +218,22 @@ def _check_sched(spec, sched):
         raise ValueError("knot schedule horizon does not match the spec")
 
 
+def _has_state_bounds(spec) -> bool:
+    return getattr(spec, "x_min", None) is not None or getattr(spec, "x_max", None) is not None
+
+
+def _scorer_code(scorer: str, spec=None) -> int:
+    """1 = condensed quadratic, unless the spec has state bounds (K/empc.py:138)."""
+    return 1 if scorer == "condensed" and (spec is None or not _has_state_bounds(spec)) else 0
+
+
 def _spec_context(spec, sched, settings, instances=1) -> _Context:
     _check_sched(spec, sched)
     n, m = spec.model.Ad.shape[0], spec.model.Bd.shape[1]
     ctx = _context(n, m, spec.T, sched.p, settings.num_sims, settings.num_parents, instances, not _is_diag(spec.Q),
                    getattr(settings, "precision", "fp32"))
     ctx.set_problems(_problem_arrays(spec))
+    ctx.h.call("empc_set_scorer", _scorer_code(getattr(settings, "scorer", "rollout"), spec))
     return ctx
 
 
@@ -263,13 +279,17 @@ def _run(ctx: _Context, settings, x0, sigma, *, init, rescore, evolves, gen0, sl
 
 class CostModel:
     """Batch scorer for one (spec, schedule, x0): the seam of
-    ``_CostModel.__call__`` (K/empc.py:122-152), evaluated by GPU rollout."""
+    ``_CostModel.__call__`` (K/empc.py:122-152), evaluated on the GPU by
+    rollout (default) or by the condensed quadratic (``scorer="condensed"``)."""
 
-    def __init__(self, spec, sched: KnotSchedule, x0, *, precision: str = "fp32"):
+    def __init__(self, spec, sched: KnotSchedule, x0, *, precision: str = "fp32", scorer: str = "rollout"):
         _check_sched(spec, sched)
+        if scorer not in ("rollout", "condensed"):
+            raise ValueError("scorer must be 'rollout' or 'condensed'")
         self.spec, self.sched = spec, sched
         self.x0 = np.asarray(x0, float)
         self.precision = precision
+        self.scorer = scorer
 
     def __call__(self, cands) -> np.ndarray:
         cands = nat.f64(cands)
@@ -277,16 +297,17 @@ class CostModel:
         n, m = self.spec.model.Ad.shape[0], self.spec.model.Bd.shape[1]
         ctx = _context(n, m, self.spec.T, self.sched.p, 1, 1, 1, not _is_diag(self.spec.Q), self.precision)
         ctx.set_problems(_problem_arrays(self.spec))
+        ctx.h.call("empc_set_scorer", _scorer_code(self.scorer, self.spec))
         costs = np.empty(N)
         ctx.h.call("empc_score", nat.dptr(nat.f64(self.x0)), N, nat.dptr(cands.reshape(N, -1)), nat.dptr(costs))
         return costs
 
 
-def evaluate_cost(candidate, spec, sched: KnotSchedule, x0, *, precision: str = "fp32") -> float:
+def evaluate_cost(candidate, spec, sched: KnotSchedule, x0, *, precision: str = "fp32", scorer: str = "rollout") -> float:
     """Full tracking cost of one knot candidate, terminal state included
     (K/empc.py:155-159), by GPU rollout."""
     U = np.asarray(getattr(candidate, "U", candidate), float).reshape(sched.p, spec.model.Bd.shape[1])
-    return float(CostModel(spec, sched, x0, precision=precision)(U[None])[0])
+    return float(CostModel(spec, sched, x0, precision=precision, scorer=scorer)(U[None])[0])
 
 
 def init_population(spec, sched: KnotSchedule, settings: EmpcSettings, x0, cost=None, *,
@@ -418,6 +439,8 @@ class EmpcBatch:
         self.ctx = _context(n, m, sched.T, sched.p, settings.num_sims, settings.num_parents, I, dense,
                             settings.precision)
         self.ctx.set_problems(self.probs)
+        self.scorer = _scorer_code(getattr(settings, "scorer", "rollout"))
+        self.ctx.h.call("empc_set_scorer", self.scorer)
 
     def sigma(self, x0s) -> np.ndarray:
         st = self.settings
@@ -440,5 +463,6 @@ class EmpcBatch:
                       slot_in=_device_population(self.ctx, prev))
             gen_end = prev.generation + st.generations
         self.ctx.set_problems(self.probs)
+        self.ctx.h.call("empc_set_scorer", self.scorer)
         slot, u, best, bc, _ = _run(self.ctx, st, x0s, self.sigma(x0s), **kw)
         return BatchResult(u, best, bc, Population(generation=gen_end, _dev=(self.ctx, slot)))
