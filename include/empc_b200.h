@@ -16,8 +16,9 @@
  *   empc_set_schedule <- KnotSchedule.coeffs / interpolation_matrix param.py:49-111
  *   empc_set_scorer   <- _CostModel's choice of scorer     empc.py:133-152 (rollout vs
  *                        condensed quadratic from build_small_param, condense.py:268-274)
- *   empc_set_scorer   <- _CostModel's choice of scorer     empc.py:133-152 (rollout vs
- *                        condensed quadratic from build_small_param, condense.py:268-274)
+ *   empc_plant_linearize_discretize <- linearize + discretize dynamics.py:241-290
+ *   empc_plant_integrate  <- integrate / rk4_step          dynamics.py:316-330
+ *                        (batched, per closed-loop period: closedloop.py:103-104)
  *   empc_set_problems <- MpcSpec + DiscreteLinearModel condense.py:42-87, dynamics.py:223-238
  *
  * Conventions: row-major arrays; every pointer argument is a HOST pointer
@@ -83,15 +84,6 @@ int empc_set_schedule(empc_handle* h, const int32_t* idx1, const int32_t* idx2, 
 #define EMPC_SCORER_CONDENSED 1
 int empc_set_scorer(empc_handle* h, int32_t scorer);
 
-/* Scorer of every subsequent run / score call:
- *   EMPC_SCORER_ROLLOUT   (0, default) FP32/FP64 horizon rollout (empc.py:85-119)
- *   EMPC_SCORER_CONDENSED (1) the reference's own condensed quadratic
- *     J(z) = z'Pz + 2q'z + c0 (empc.py:133-152), built on the device once per
- *     run in FP64 and evaluated in FP64 (costs rounded to the population
- *     precision).  Not for state-bounded specs (the reference rolls those out). */
-#define EMPC_SCORER_ROLLOUT 0
-#define EMPC_SCORER_CONDENSED 1
-int empc_set_scorer(empc_handle* h, int32_t scorer);
 
 /* Problems of instances [first, first+count).  Per instance, contiguous:
  * Ad[n*n] Bd[n*m] wd[n] Q[n*n] R[m*m] x_goal[n] u_goal[m] u_min[m] u_max[m]. */
@@ -193,6 +185,38 @@ int empc_shard_import(empc_handle* h, const void* dev_all, int32_t world, double
                       double* best_cost, int64_t* best_row);
 int empc_shard_evolve(empc_handle* h, const empc_run_args* args);
 int empc_shard_read(empc_handle* h, double* cands, double* costs);
+
+/* Batched plant linearization + discretization on the device:
+ * for each of `count` operating points (x[i], u[i]) of one plant, the
+ * central-difference Jacobians of the plant ODE with step eps and the affine
+ * residual (dynamics.py:241-262), then the zero-order-hold discretization
+ * exp([[A B w],[0 0 0]] dt) (EMPC_DISCRETIZE_EXACT) or I + A dt, B dt, w dt
+ * (EMPC_DISCRETIZE_EULER) (dynamics.py:265-290).  Plants: the torque pendulum
+ * (dynamics.py:33-75; n = 2, m = 1, mass/length arrays of length 1) and the
+ * planar N-link chain with tip masses (dynamics.py:90-199; n = 2 links,
+ * m = links, links <= 64).  Host arrays: x [count][n], u [count][m] in;
+ * Ad [count][n][n], Bd [count][n][m], wd [count][n] out.  No handle; errors
+ * through empc_plant_last_error(). */
+#define EMPC_PLANT_PENDULUM 0
+#define EMPC_PLANT_NLINK 1
+#define EMPC_DISCRETIZE_EXACT 0
+#define EMPC_DISCRETIZE_EULER 1
+typedef struct {
+  int32_t kind;          /* EMPC_PLANT_* */
+  int32_t links;         /* N-link: number of links; pendulum: 1 */
+  const double* mass;    /* [links] tip masses (pendulum: [1]) */
+  const double* length;  /* [links] link lengths */
+  double damping;        /* joint viscous damping */
+  double gravity;
+} empc_plant;
+int empc_plant_linearize_discretize(const empc_plant* plant, int32_t count, const double* x, const double* u,
+                                    double eps, double dt, int32_t method, int32_t device, double* Ad, double* Bd,
+                                    double* wd);
+/* RK4 integration of one zero-order-hold period of the same plants
+ * (dynamics.py:316-330): x_out[i] = integrate(f, x[i], u[i], dt, substeps). */
+int empc_plant_integrate(const empc_plant* plant, int32_t count, const double* x, const double* u, double dt,
+                         int32_t substeps, int32_t device, double* x_out);
+const char* empc_plant_last_error(void);
 
 /* Known-answer seam for the in-kernel counter-based RNG: Philox4x32-10 of
  * `count` (ctr[4], key[2]) pairs evaluated on the device. */

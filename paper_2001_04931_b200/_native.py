@@ -26,7 +26,11 @@ EXPORTS = (
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
     "empc_set_variant", "empc_set_occupancy", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
     "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read",
+    "empc_plant_linearize_discretize", "empc_plant_integrate", "empc_plant_last_error",
 )
+
+EMPC_PLANT_PENDULUM, EMPC_PLANT_NLINK = 0, 1
+EMPC_DISCRETIZE_EXACT, EMPC_DISCRETIZE_EULER = 0, 1
 
 
 class empc_dims(C.Structure):
@@ -63,6 +67,11 @@ class empc_run_args(C.Structure):
         ("best_cost", C.POINTER(C.c_double)),
         ("best_index", C.POINTER(C.c_int32)),
     ]
+
+
+class empc_plant(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("links", C.c_int32), ("mass", C.POINTER(C.c_double)),
+                ("length", C.POINTER(C.c_double)), ("damping", C.c_double), ("gravity", C.c_double)]
 
 
 _lib = None
@@ -110,6 +119,10 @@ def load(path: str | None = None):
         "empc_shard_import": (C.c_int, [P, P, I32, D, D, D, C.POINTER(I64)]),
         "empc_shard_evolve": (C.c_int, [P, C.POINTER(empc_run_args)]),
         "empc_shard_read": (C.c_int, [P, D, D]),
+        "empc_plant_linearize_discretize": (C.c_int, [C.POINTER(empc_plant), I32, D, D, C.c_double, C.c_double,
+                                                      I32, I32, D, D, D]),
+        "empc_plant_integrate": (C.c_int, [C.POINTER(empc_plant), I32, D, D, C.c_double, I32, I32, D]),
+        "empc_plant_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -194,3 +207,41 @@ def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
     P = C.POINTER(C.c_uint32)
     check(lib.empc_philox(ctr.ctypes.data_as(P), key.ctypes.data_as(P), ctr.shape[0], out.ctypes.data_as(P)))
     return out
+
+
+def plant_integrate(kind, links, mass, length, damping, gravity, xs, us, dt, substeps, device=0):
+    """Batched device RK4 period of the plant (include/empc_b200.h)."""
+    import numpy as np
+
+    lib = load()
+    mass, length = f64(mass), f64(length)
+    pl = empc_plant(kind, links, dptr(mass), dptr(length), float(damping), float(gravity))
+    xs, us = f64(xs), f64(us)
+    out = np.empty_like(xs)
+    rc = lib.empc_plant_integrate(C.byref(pl), xs.shape[0], dptr(xs), dptr(us), float(dt), int(substeps),
+                                  int(device), dptr(out))
+    if rc != EMPC_OK:
+        msg = lib.empc_plant_last_error().decode()
+        raise (ValueError if rc == EMPC_EINVAL else RuntimeError)(msg)
+    return out
+
+
+def plant_linearize_discretize(kind, links, mass, length, damping, gravity, xs, us, eps, dt, method, device=0):
+    """Batched device linearize + discretize (include/empc_b200.h)."""
+    import numpy as np
+
+    lib = load()
+    mass, length = f64(mass), f64(length)
+    pl = empc_plant(kind, links, dptr(mass), dptr(length), float(damping), float(gravity))
+    xs, us = f64(xs), f64(us)
+    cnt, n = xs.shape
+    m = us.shape[1]
+    Ad = np.empty((cnt, n, n))
+    Bd = np.empty((cnt, n, m))
+    wd = np.empty((cnt, n))
+    rc = lib.empc_plant_linearize_discretize(C.byref(pl), cnt, dptr(xs), dptr(us), float(eps), float(dt),
+                                             int(method), int(device), dptr(Ad), dptr(Bd), dptr(wd))
+    if rc != EMPC_OK:
+        msg = lib.empc_plant_last_error().decode()
+        raise (ValueError if rc == EMPC_EINVAL else RuntimeError)(msg)
+    return Ad, Bd, wd

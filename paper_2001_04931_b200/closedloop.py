@@ -32,7 +32,8 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
-from .dynamics import NLinkParams, PendulumParams, discretize, integrate, linearize
+from .dynamics import DiscreteLinearModel, NLinkArm, NLinkParams, Pendulum, PendulumParams, discretize, integrate, \
+    integrate_batch, linearize, linearize_discretize
 from .empc import EmpcBatch, EmpcSettings, solve_empc
 from .param import KnotSchedule
 
@@ -69,14 +70,17 @@ class SimResult:
 
 def run_closed_loop(plant, controller: Controller, template, x0, x_goal, duration: float, rate: float, *,
                     controller_plant=None, qp_settings=None, plant_substeps: int = 10,
-                    _draws=None) -> SimResult:
+                    device_model: bool = False, _draws=None) -> SimResult:
     """Simulate ``duration`` s of EMPC at ``rate`` Hz (K/closedloop.py:59-133).
 
     ``controller_plant`` (default: the true plant) is only ever linearized.
     Linearization and discretization are excluded from the timing columns
     (K/closedloop.py:76-79).  ``_draws(generation0, evolves, init)`` -> (init
     candidates or None, list of per-evolve draws) is the parity seam that
-    replays the reference's random tensors.
+    replays the reference's random tensors.  ``device_model=True`` (an
+    extension) relinearizes and discretizes a ``Pendulum`` / ``NLinkArm``
+    controller model on the GPU (``dynamics.linearize_discretize``, SURVEY §8
+    f3) instead of the host ``linearize`` + ``expm``.
     """
     if controller.kind != "empc":
         raise NotImplementedError(f"controller kind {controller.kind!r} is a QP solver outside the B200 EMPC path")
@@ -95,7 +99,12 @@ def run_closed_loop(plant, controller: Controller, template, x0, x_goal, duratio
     population = None
     x = states[0].copy()
     for i in range(H):
-        spec = replace(template, model=discretize(linearize(model_src.ode, x, u_nom), dt, "exact"), x_goal=x_goal)
+        if device_model:
+            Ad, Bd, wd = linearize_discretize(model_src, x[None], None, dt, "exact")
+            model = DiscreteLinearModel(Ad[0], Bd[0], wd[0], dt)
+        else:
+            model = discretize(linearize(model_src.ode, x, u_nom), dt, "exact")
+        spec = replace(template, model=model, x_goal=x_goal)
         kw = {}
         if _draws is not None:
             cold = population is None
@@ -119,11 +128,15 @@ class ClosedLoopFleet:
     a process pool of ``run_closed_loop`` calls).
 
     ``plants`` and ``x_goals`` are per instance; all share ``template``'s
-    T/Q/R/bounds and one schedule.  The populations stay on the GPU.
+    T/Q/R/bounds and one schedule.  The populations stay on the GPU.  When
+    every controller model is the same ``Pendulum`` / ``NLinkArm`` the
+    relinearization + discretization of all instances runs as one batched
+    device call (``dynamics.linearize_discretize``) instead of
+    I host ``linearize`` + ``expm`` calls.
     """
 
     def __init__(self, plants, controller: Controller, template, x_goals, rate: float, *, controller_plants=None,
-                 plant_substeps: int = 10):
+                 plant_substeps: int = 10, device_models: bool = True):
         if controller.kind != "empc":
             raise NotImplementedError("ClosedLoopFleet runs EMPC controllers only")
         self.plants = list(plants)
@@ -135,16 +148,26 @@ class ClosedLoopFleet:
         self.substeps = plant_substeps
         self.population = None
         self.batch = None
+        def uniform(ps):
+            return isinstance(ps[0], (Pendulum, NLinkArm)) and all(
+                type(q) is type(ps[0]) and (q is ps[0] or _same_params(q.params, ps[0].params)) for q in ps)
+
+        self.device_models = device_models and uniform(self.models)
+        self.device_plants = device_models and uniform(self.plants)
 
     def _problems(self, xs):
         dt = 1.0 / self.rate
         t = self.template
-        mods = [discretize(linearize(mdl.ode, x, np.zeros(mdl.m)), dt, "exact") for mdl, x in zip(self.models, xs)]
         I = self.I
+        if self.device_models:
+            Ad, Bd, wd = linearize_discretize(self.models[0], xs, None, dt, "exact")
+        else:
+            mods = [discretize(linearize(mdl.ode, x, np.zeros(mdl.m)), dt, "exact") for mdl, x in zip(self.models, xs)]
+            Ad, Bd, wd = (np.stack([d.Ad for d in mods]), np.stack([d.Bd for d in mods]),
+                          np.stack([d.wd for d in mods]))
         bc = lambda v, shape: np.broadcast_to(np.asarray(v, float), shape)  # noqa: E731
         n, m = self.plants[0].n, self.plants[0].m
-        return {"Ad": np.stack([d.Ad for d in mods]), "Bd": np.stack([d.Bd for d in mods]),
-                "wd": np.stack([d.wd for d in mods]), "Q": bc(t.Q, (I, n, n)), "R": bc(t.R, (I, m, m)),
+        return {"Ad": Ad, "Bd": Bd, "wd": wd, "Q": bc(t.Q, (I, n, n)), "R": bc(t.R, (I, m, m)),
                 "x_goal": self.x_goals, "u_goal": bc(t.u_goal, (I, m)), "u_min": bc(t.u_min, (I, m)),
                 "u_max": bc(t.u_max, (I, m))}
 
@@ -162,8 +185,11 @@ class ClosedLoopFleet:
         dt_solve = time.perf_counter() - t0
         self.population = r.population
         u = np.clip(r.u, probs["u_min"], probs["u_max"])
-        nxt = np.stack([integrate(pl.ode, x, ui, 1.0 / self.rate, substeps=self.substeps)
-                        for pl, x, ui in zip(self.plants, xs, u)])
+        if self.device_plants:
+            nxt = integrate_batch(self.plants[0], xs, u, 1.0 / self.rate, self.substeps)
+        else:
+            nxt = np.stack([integrate(pl.ode, x, ui, 1.0 / self.rate, substeps=self.substeps)
+                            for pl, x, ui in zip(self.plants, xs, u)])
         return nxt, u, dt_solve
 
     def run(self, x0s, duration: float) -> list[SimResult]:
@@ -178,6 +204,13 @@ class ClosedLoopFleet:
             states[:, i + 1] = x
             inputs[:, i] = u
         return [SimResult(states[k], inputs[k], tm.copy(), tm.copy(), 0) for k in range(self.I)]
+
+
+def _same_params(a, b) -> bool:
+    for f in ("mass", "length", "damping", "gravity"):
+        if not np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(b, f))):
+            return False
+    return True
 
 
 # ---------------------------------------------------------------------------

@@ -562,7 +562,11 @@ class Engine final : public EngineBase {
   // configuration does not qualify and the per-generation launches are used.
   template <typename Pre, typename Post>
   bool try_persistent(const empc_run_args& r, bool timed, Pre& pre, Post& post) {
-    if (!persist_enabled_ || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K)
+    // small problems (n <= 16: C1, C2) run faster as per-generation launches
+    // with several small CTAs per SM (profiles/bench_c1/c2): persistent only
+    // from NP = 24
+    if (!persist_enabled_ || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K ||
+        (d_.NP < 24 && forced_ < 0))
       return false;
     const Variant<S>& v = pick();
     const PersistVariant<S>* pv = nullptr;

@@ -207,3 +207,56 @@ def integrate(f, x, u, dt: float, substeps: int = 10) -> np.ndarray:
     for _ in range(substeps):
         x = rk4_step(f, x, u, h)
     return x
+
+
+def linearize_discretize(plant, xs, us=None, dt: float = 0.01, method: str = "exact", eps: float = 1e-6,
+                         device: int = 0):
+    """Batched ``discretize(linearize(plant.ode, x, u, eps), dt, method)`` on
+    the GPU (K/dynamics.py:241-290): one CTA per operating point
+    computes the central-difference Jacobians of the plant ODE and the
+    zero-order-hold exponential of the augmented matrix in FP64.
+
+    ``plant`` is a ``Pendulum`` or an ``NLinkArm`` (the reference's plant
+    models; an arbitrary Python callable cannot run on the device -- use
+    ``linearize`` / ``discretize`` for those).  ``xs`` is (I, n), ``us`` (I, m)
+    (default zeros, the closed loop's nominal input).  Returns stacked
+    ``(Ad (I,n,n), Bd (I,n,m), wd (I,n))``.
+    """
+    from . import _native as nat
+
+    if method not in ("exact", "euler"):
+        raise ValueError(f"unknown discretization method {method!r}")
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    dev_plant = _device_plant(plant)
+    xs = np.atleast_2d(np.asarray(xs, float))
+    us = np.zeros((xs.shape[0], plant.m)) if us is None else np.atleast_2d(np.asarray(us, float))
+    if xs.shape[1] != plant.n or us.shape != (xs.shape[0], plant.m):
+        raise ValueError("xs must be (I, n) and us (I, m)")
+    meth = nat.EMPC_DISCRETIZE_EXACT if method == "exact" else nat.EMPC_DISCRETIZE_EULER
+    return nat.plant_linearize_discretize(*dev_plant, xs, us, eps, dt, meth, device)
+
+
+def _device_plant(plant):
+    """(kind, links, mass, length, damping, gravity) of a plant the device knows."""
+    from . import _native as nat
+
+    if isinstance(plant, Pendulum):
+        p = plant.params
+        return nat.EMPC_PLANT_PENDULUM, 1, [p.mass], [p.length], p.damping, p.gravity
+    if isinstance(plant, NLinkArm):
+        p = plant.params
+        return nat.EMPC_PLANT_NLINK, p.links, p.mass, p.length, p.damping, p.gravity
+    raise TypeError(f"no device model for plant type {type(plant).__name__}")
+
+
+def integrate_batch(plant, xs, us, dt: float, substeps: int = 10, device: int = 0) -> np.ndarray:
+    """``integrate(plant.ode, x, u, dt, substeps)`` for every row of ``xs`` /
+    ``us`` on the GPU, one warp per instance (K/dynamics.py:316-330)."""
+    from . import _native as nat
+
+    xs = np.atleast_2d(np.asarray(xs, float))
+    us = np.atleast_2d(np.asarray(us, float))
+    if xs.shape[1] != plant.n or us.shape != (xs.shape[0], plant.m):
+        raise ValueError("xs must be (I, n) and us (I, m)")
+    return nat.plant_integrate(*_device_plant(plant), xs, us, dt, substeps, device)
