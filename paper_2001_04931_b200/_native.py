@@ -9,6 +9,7 @@ raises immediately.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 
@@ -40,11 +41,11 @@ class empc_dims(C.Structure):
 
 class empc_injected(C.Structure):
     _fields_ = [
-        ("init", C.POINTER(C.c_double)),
-        ("parents", C.POINTER(C.c_int32)),
-        ("take_second", C.POINTER(C.c_uint8)),
-        ("mutate", C.POINTER(C.c_uint8)),
-        ("noise", C.POINTER(C.c_double)),
+        ("init", C.c_void_p),
+        ("parents", C.c_void_p),
+        ("take_second", C.c_void_p),
+        ("mutate", C.c_void_p),
+        ("noise", C.c_void_p),
     ]
 
 
@@ -59,19 +60,19 @@ class empc_run_args(C.Structure):
         ("seed", C.c_uint64),
         ("mutation_prob", C.c_double),
         ("crossover_prob", C.c_double),
-        ("x0", C.POINTER(C.c_double)),
-        ("sigma", C.POINTER(C.c_double)),
+        ("x0", C.c_void_p),
+        ("sigma", C.c_void_p),
         ("inject", C.POINTER(empc_injected)),
-        ("u_out", C.POINTER(C.c_double)),
-        ("best_out", C.POINTER(C.c_double)),
-        ("best_cost", C.POINTER(C.c_double)),
-        ("best_index", C.POINTER(C.c_int32)),
+        ("u_out", C.c_void_p),
+        ("best_out", C.c_void_p),
+        ("best_cost", C.c_void_p),
+        ("best_index", C.c_void_p),
     ]
 
 
 class empc_plant(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("links", C.c_int32), ("mass", C.POINTER(C.c_double)),
-                ("length", C.POINTER(C.c_double)), ("damping", C.c_double), ("gravity", C.c_double)]
+    _fields_ = [("kind", C.c_int32), ("links", C.c_int32), ("mass", C.c_void_p),
+                ("length", C.c_void_p), ("damping", C.c_double), ("gravity", C.c_double)]
 
 
 _lib = None
@@ -89,12 +90,12 @@ def load(path: str | None = None):
             f"{path} is missing: build the CUDA extension first "
             "(python -c 'import __graft_entry__ as g; g.build()')")
     lib = C.CDLL(path)
-    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_void_p  # data pointers as void*
     sig = {
         "empc_create": (C.c_int, [C.POINTER(empc_dims), C.POINTER(P)]),
         "empc_destroy": (None, [P]),
         "empc_last_error": (C.c_char_p, [P]),
-        "empc_set_schedule": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), D]),
+        "empc_set_schedule": (C.c_int, [P, P, P, D]),
         "empc_set_scorer": (C.c_int, [P, C.c_int32]),
         "empc_set_problems": (C.c_int, [P, I32, I32] + [D] * 9),
         "empc_pop_alloc": (C.c_int, [P, C.POINTER(I32)]),
@@ -103,7 +104,7 @@ def load(path: str | None = None):
         "empc_pop_write": (C.c_int, [P, I32, D, D]),
         "empc_run": (C.c_int, [P, C.POINTER(empc_run_args)]),
         "empc_score": (C.c_int, [P, D, I32, D, D]),
-        "empc_select": (C.c_int, [P, D, C.POINTER(I32), C.POINTER(I32)]),
+        "empc_select": (C.c_int, [P, D, P, P]),
         "empc_expand": (C.c_int, [P, I32, D, D]),
         "empc_time_device": (C.c_int, [P, C.POINTER(empc_run_args), I32, I32, C.POINTER(C.c_float),
                                         C.POINTER(C.c_float), C.POINTER(I32), C.POINTER(I32)]),
@@ -111,7 +112,7 @@ def load(path: str | None = None):
         "empc_num_variants": (C.c_int, [P, C.POINTER(I32)]),
         "empc_set_variant": (C.c_int, [P, I32]),
         "empc_set_occupancy": (C.c_int, [P, I32]),
-        "empc_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), I32, C.POINTER(C.c_uint32)]),
+        "empc_philox": (C.c_int, [P, P, I32, P]),
         "empc_shard_setup": (C.c_int, [P, I64, I32, I64, I32, I32]),
         "empc_shard_entry_bytes": (C.c_int, [P, C.POINTER(I64)]),
         "empc_shard_init": (C.c_int, [P, C.POINTER(empc_run_args)]),
@@ -141,16 +142,18 @@ def check(rc: int, handle=None):
     raise RuntimeError(f"empc error {rc}: {msg}")
 
 
+# Data pointers cross the ABI as void*.  The arrays behind them are kept
+# alive for the next few hundred conversions, so a temporary such as
+# dptr(f64(x)) outlives the call it is passed to.
+_keep = collections.deque(maxlen=512)
+
+
 def dptr(a: np.ndarray):
-    return a.ctypes.data_as(C.POINTER(C.c_double))
+    _keep.append(a)
+    return C.c_void_p(a.ctypes.data)
 
 
-def iptr(a: np.ndarray):
-    return a.ctypes.data_as(C.POINTER(C.c_int32))
-
-
-def u8ptr(a: np.ndarray):
-    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+iptr = u8ptr = u32ptr = dptr
 
 
 def f64(a) -> np.ndarray:
@@ -204,8 +207,7 @@ def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
     ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
     key = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
     out = np.empty_like(ctr)
-    P = C.POINTER(C.c_uint32)
-    check(lib.empc_philox(ctr.ctypes.data_as(P), key.ctypes.data_as(P), ctr.shape[0], out.ctypes.data_as(P)))
+    check(lib.empc_philox(dptr(ctr), dptr(key), ctr.shape[0], dptr(out)))
     return out
 
 

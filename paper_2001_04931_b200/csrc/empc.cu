@@ -694,7 +694,9 @@ class Engine final : public EngineBase {
     return cur;
   }
 
-  void stage_run(const empc_run_args& r) {
+  // host staging of a run; `copies` = false leaves the H2D copies to the
+  // captured graph (graph_for(r, true))
+  void stage_run(const empc_run_args& r, bool copies = true) {
     if (!have_sched_) throw InvalidArg{"schedule not set"};
     if (!have_prob_) throw InvalidArg{"problem not set"};
     if (!r.x0 || !r.sigma) throw InvalidArg{"x0 and sigma are required"};
@@ -711,11 +713,7 @@ class Engine final : public EngineBase {
     run_h_->gen0 = r.generation0;
     run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 32));
     run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 32));
-    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice,
-                       stream_));
-    const size_t state_bytes =
-        reinterpret_cast<uintptr_t>(run_h_ + 1) - reinterpret_cast<uintptr_t>(stage_state_h_);
-    CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
+    if (copies) enqueue_h2d();
     if (!r.init) {
       Slot& s = slot(r.slot_in);
       CK(cudaMemcpyAsync(pop_[0], s.cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice, stream_));
@@ -723,8 +721,24 @@ class Engine final : public EngineBase {
     }
   }
 
-  cudaGraphExec_t graph_for(const empc_run_args& r) {
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_);
+  void enqueue_h2d() {
+    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice,
+                       stream_));
+    const size_t state_bytes =
+        reinterpret_cast<uintptr_t>(run_h_ + 1) - reinterpret_cast<uintptr_t>(stage_state_h_);
+    CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
+  }
+
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool>;
+  GKey gkey(const empc_run_args& r, bool io) const {
+    return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io);
+  }
+
+  // One graph per run shape.  io = true also captures the staging H2D copies
+  // (pinned host -> device) before and the result D2H after the solve: the
+  // public-API run is then one graph launch, two slot copies and one sync.
+  cudaGraphExec_t graph_for(const empc_run_args& r, bool io = false) {
+    const GKey key = gkey(r, io);
     auto it = graphs_.find(key);
     if (it != graphs_.end()) return it->second;
     if (scorer_ == 1) ensure_cond_ws();
@@ -732,7 +746,10 @@ class Engine final : public EngineBase {
     CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     int cur = 0;
     try {
+      if (io) enqueue_h2d();
       cur = enqueue_core(r, nullptr);
+      if (io)
+        CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
     } catch (...) {
       cudaStreamEndCapture(stream_, &g);
       throw;
@@ -749,7 +766,7 @@ class Engine final : public EngineBase {
   }
 
   void run(const empc_run_args& r) override {
-    stage_run(r);
+    stage_run(r, r.inject != nullptr);
     int cur;
     std::vector<S> init_cast;
     if (r.inject) {
@@ -784,9 +801,10 @@ class Engine final : public EngineBase {
       CK(cudaStreamSynchronize(stream_));
       for (void* p : {d_init, d_par, d_tk, d_mu, d_nz})
         if (p) cudaFree(p);
+      CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
     } else {
-      cudaGraphExec_t ge = graph_for(r);
-      cur = graph_cur_[std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_)];
+      cudaGraphExec_t ge = graph_for(r, true);
+      cur = graph_cur_[gkey(r, true)];
       CK(cudaGraphLaunch(ge, stream_));
     }
     if (r.slot_out >= 0) {
@@ -794,7 +812,6 @@ class Engine final : public EngineBase {
       CK(cudaMemcpyAsync(s.cands, pop_[cur], sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice, stream_));
       CK(cudaMemcpyAsync(s.costs, cost_[cur], sizeof(S) * (size_t)I_ * d_.N, cudaMemcpyDeviceToDevice, stream_));
     }
-    CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
     CK(cudaStreamSynchronize(stream_));
     const int m = d_.m, pm = d_.pm;
     for (int i = 0; i < I_; ++i) {
@@ -860,7 +877,7 @@ class Engine final : public EngineBase {
                    int32_t* nlaunch) override {
     stage_run(r);
     cudaGraphExec_t ge = graph_for(r);
-    const auto key = std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_);
+    const GKey key = gkey(r, false);
     if (flush && !flush_) {
       flush_n_ = (size_t)256 << 20 >> 4;  // 256 MiB > 126 MB L2
       CK(cudaMalloc(&flush_, flush_n_ * 16));
@@ -1135,7 +1152,6 @@ class Engine final : public EngineBase {
   uint4* flush_ = nullptr;
   size_t flush_n_ = 0;
   std::vector<cudaEvent_t> ev_;
-  using GKey = std::tuple<bool, bool, int, int, bool, int, int>;
   std::map<GKey, cudaGraphExec_t> graphs_;
   std::map<GKey, int> graph_cur_, graph_launches_, graph_rollouts_;
   int launches_ = 0, rollout_launches_ = 0;

@@ -23,7 +23,6 @@ There is no CPU fallback: a missing CUDA library raises.
 
 from __future__ import annotations
 
-import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -141,10 +140,14 @@ class _Slot:
     """A device population slot, returned to its context's free list when the
     owning Population dies."""
 
-    __slots__ = ("id", "__weakref__")
+    __slots__ = ("id", "_free")
 
-    def __init__(self, sid):
+    def __init__(self, sid, free):
         self.id = sid
+        self._free = free
+
+    def __del__(self):
+        self._free.append(self.id)
 
 
 class _Context:
@@ -157,6 +160,12 @@ class _Context:
                     nat.dptr(np.ascontiguousarray(c)))
         self.free = []
         self.args = nat.empc_run_args()
+        self.scorer = 0
+
+    def set_scorer(self, code: int):
+        if code != self.scorer:
+            self.h.call("empc_set_scorer", int(code))
+            self.scorer = code
 
     def slot(self) -> _Slot:
         if self.free:
@@ -165,8 +174,7 @@ class _Context:
             v = nat.C.c_int32()
             self.h.call("empc_pop_alloc", nat.C.byref(v))
             sid = v.value
-        s = _Slot(sid)
-        weakref.finalize(s, self.free.append, sid)
+        s = _Slot(sid, self.free)
         return s
 
     def set_problems(self, probs):
@@ -233,7 +241,7 @@ def _spec_context(spec, sched, settings, instances=1) -> _Context:
     ctx = _context(n, m, spec.T, sched.p, settings.num_sims, settings.num_parents, instances, not _is_diag(spec.Q),
                    getattr(settings, "precision", "fp32"))
     ctx.set_problems(_problem_arrays(spec))
-    ctx.h.call("empc_set_scorer", _scorer_code(getattr(settings, "scorer", "rollout"), spec))
+    ctx.set_scorer(_scorer_code(getattr(settings, "scorer", "rollout"), spec))
     return ctx
 
 
@@ -297,7 +305,7 @@ class CostModel:
         n, m = self.spec.model.Ad.shape[0], self.spec.model.Bd.shape[1]
         ctx = _context(n, m, self.spec.T, self.sched.p, 1, 1, 1, not _is_diag(self.spec.Q), self.precision)
         ctx.set_problems(_problem_arrays(self.spec))
-        ctx.h.call("empc_set_scorer", _scorer_code(self.scorer, self.spec))
+        ctx.set_scorer(_scorer_code(self.scorer, self.spec))
         costs = np.empty(N)
         ctx.h.call("empc_score", nat.dptr(nat.f64(self.x0)), N, nat.dptr(cands.reshape(N, -1)), nat.dptr(costs))
         return costs
@@ -440,7 +448,7 @@ class EmpcBatch:
                             settings.precision)
         self.ctx.set_problems(self.probs)
         self.scorer = _scorer_code(getattr(settings, "scorer", "rollout"))
-        self.ctx.h.call("empc_set_scorer", self.scorer)
+        self.ctx.set_scorer(self.scorer)
 
     def sigma(self, x0s) -> np.ndarray:
         st = self.settings
@@ -463,6 +471,6 @@ class EmpcBatch:
                       slot_in=_device_population(self.ctx, prev))
             gen_end = prev.generation + st.generations
         self.ctx.set_problems(self.probs)
-        self.ctx.h.call("empc_set_scorer", self.scorer)
+        self.ctx.set_scorer(self.scorer)
         slot, u, best, bc, _ = _run(self.ctx, st, x0s, self.sigma(x0s), **kw)
         return BatchResult(u, best, bc, Population(generation=gen_end, _dev=(self.ctx, slot)))

@@ -30,3 +30,46 @@ for _ in range(200):
     P.solve_empc(specs[0], sched, st, x0s[0])
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# breakdown: public API vs bare empc_run vs device time
+import ctypes as C  # noqa: E402
+
+from paper_2001_04931_b200 import _native as nat  # noqa: E402
+from paper_2001_04931_b200 import empc as E  # noqa: E402
+
+ctx = E._spec_context(specs[0], sched, st)
+sigma = E._mutation_sigma(specs[0], st, x0s[0])
+a = nat.empc_run_args()
+x0c, sg = nat.f64(x0s[0][None]), nat.f64(sigma[None])
+u = np.empty((1, w.m)) if False else None
+import numpy as np  # noqa: E402
+
+u, best, bc, bi = np.empty((1, w.m)), np.empty((1, w.p, w.m)), np.empty(1), np.empty(1, np.int32)
+slot = ctx.slot()
+a.init, a.rescore, a.evolves, a.slot_in, a.slot_out = 1, 0, w.G - 1, -1, slot.id
+a.generation0, a.seed, a.mutation_prob, a.crossover_prob = 1, st.seed, st.mutation_prob, st.crossover_prob
+a.x0, a.sigma = nat.dptr(x0c), nat.dptr(sg)
+a.u_out, a.best_out, a.best_cost, a.best_index = nat.dptr(u), nat.dptr(best), nat.dptr(bc), nat.iptr(bi)
+for variant in ("slot", "noslot"):
+    a.slot_out = slot.id if variant == "slot" else -1
+    tt = []
+    for _ in range(300):
+        t0 = time.perf_counter()
+        ctx.h.call("empc_run", C.byref(a))
+        tt.append(time.perf_counter() - t0)
+    tt.sort()
+    print(f"bare empc_run ({variant}) median {tt[len(tt)//2]*1e3:.4f} ms")
+ms = (C.c_float * 100)()
+ctx.h.call("empc_time_device", C.byref(a), 100, 0, ms, None, None, None)
+v = sorted(ms)
+print(f"device (graph, no flush) median {v[50]:.4f} ms")
+ctx.h.call("empc_time_device", C.byref(a), 100, 1, ms, None, None, None)
+v = sorted(ms)
+print(f"device (graph, L2 flushed) median {v[50]:.4f} ms")
+tt = []
+for _ in range(300):
+    t0 = time.perf_counter()
+    E._spec_context(specs[0], sched, st)
+    tt.append(time.perf_counter() - t0)
+tt.sort()
+print(f"_spec_context median {tt[150]*1e6:.1f} us")
