@@ -179,9 +179,37 @@ def closed_loop():
     print("wrote closed-loop fixtures")
 
 
+def harness():
+    """Rows of the reference harness (K/bench.py) for small EMPC configs, timing
+    columns masked: the f4 parity fixtures."""
+    sys.path.insert(0, REF)
+    from knotmpc import bench as B
+
+    cl = B.ExperimentConfig(experiment="closedloop_comparison", robot="nlink", links=(1, 2), T=20,
+                            controllers=("empc:3:1", "empc:3:2"), trials=2, duration=0.2, rate=100.0, seed=7,
+                            empc_sims=64, empc_parents=8, out="x.csv")
+    st = B.ExperimentConfig(experiment="solve_time_scaling", robot="nlink", links=(1, 3), T=20,
+                            controllers=("empc:3:2",), trials=2, rate=100.0, seed=11, empc_sims=64, empc_parents=8,
+                            out="y.csv")
+    pe = B.ExperimentConfig(experiment="closedloop_comparison", robot="pendulum", T=20,
+                            controllers=("empc:2:2",), trials=2, duration=0.2, rate=100.0, seed=3, empc_sims=64,
+                            empc_parents=8, out="z.csv")
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        for name, cfg in (("closedloop", cl), ("solvetime", st), ("pendulum", pe)):
+            rows = B.run_experiment(cfg, d, workers=1)
+            with open(os.path.join(OUT, f"harness_{name}.csv"), "w") as fh:
+                fh.write(B.rows_to_csv_text(rows, include_timing=False))
+    print("wrote harness fixtures")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["closedloop"]:
         closed_loop()
+    elif sys.argv[1:] == ["harness"]:
+        harness()
     else:
         main()
         closed_loop()
+        harness()

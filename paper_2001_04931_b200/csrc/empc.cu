@@ -605,6 +605,11 @@ class Engine final : public EngineBase {
     a.pop_in = pop_[0]; a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
     a.elite_idx = elite_; a.run = run_d_;
     a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
+    if (phases_ && (size_t)grid * 16 <= dbg_n_) {
+      CK(cudaMemsetAsync(dbg_, 0, (size_t)grid * 16 * 8, stream_));
+      a.dbg = dbg_;
+      dbg_ctas_ = grid;
+    }
     P.evolves = r.evolves;
     P.tile_evolve = Le.tile;
     P.incremental = incremental_ ? 1 : 0;
@@ -931,6 +936,19 @@ class Engine final : public EngineBase {
         std::fprintf(stderr, " %s=%.2f", names[q], mean);
       }
       std::fprintf(stderr, "\n");
+      // persistent kernel: the last generation's selection (marks 13-15)
+      double w1 = 0, w2 = 0, w3 = 0;
+      int cnt = 0;
+      for (int c = 0; c < dbg_ctas_; ++c) {
+        const unsigned long long* q = &t[(size_t)c * 16];
+        if (q[13] == 0 || q[14] == 0 || q[15] == 0) continue;
+        w1 += (double)(q[14] - q[13]) * 1e-3;
+        w2 += (double)(q[15] - q[14]) * 1e-3;
+        w3 += (double)(q[0] - q[15]) * 1e-3;
+        ++cnt;
+      }
+      if (cnt) std::fprintf(stderr, "persist(us, mean over %d CTAs): sync_before_select=%.2f select=%.2f sync_after=%.2f\n",
+                            cnt, w1 / cnt, w2 / cnt, w3 / cnt);
     }
   }
 

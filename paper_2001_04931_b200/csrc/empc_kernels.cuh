@@ -1059,11 +1059,14 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(a, true, P.scratch);
   int cur = 0;
   for (int g = 0; g < P.evolves; ++g) {
+    EMPC_MARK(13)
     grid.sync();
+    EMPC_MARK(14)
     const int inc = (g > 0 && P.incremental) ? 1 : 0;
     select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
                    (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
                    P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+    EMPC_MARK(15)
     grid.sync();
     RolloutArgs<S> b = a;
     b.mode = kBreedPhilox;
