@@ -716,8 +716,8 @@ class Engine final : public EngineBase {
     }
     run_h_->seed = r.seed;
     run_h_->gen0 = r.generation0;
-    run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 32));
-    run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 32));
+    run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 16));
+    run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 16));
     if (copies) enqueue_h2d();
     if (!r.init) {
       Slot& s = slot(r.slot_in);

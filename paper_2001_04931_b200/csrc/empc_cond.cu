@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(512) cond_score_kernel(const RolloutArgs<S> a)
   unsigned char* ptr = smem_raw;
   S* UsT = reinterpret_cast<S*>(ptr); ptr += cs.us;
   int* src = reinterpret_cast<int*>(ptr); ptr += cs.src;
-  uint32_t* tbits = reinterpret_cast<uint32_t*>(ptr); ptr += cs.bits;
+  uint8_t* tbits = reinterpret_cast<uint8_t*>(ptr); ptr += cs.bits;
   S* cumin = reinterpret_cast<S*>(ptr);
   S* cumax = cumin + m;
   S* csig = cumax + m; ptr += cs.vec;

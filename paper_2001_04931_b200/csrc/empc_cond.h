@@ -91,7 +91,7 @@ __host__ __device__ inline CondSmem cond_smem(int pm, int m, int tileP, int nthr
   c.nslices = nthreads / ncg;
   c.us = al((size_t)c.pmS * c.tPS * sizeof(S));  // rows [pm, pmS) stay zero
   c.src = al((size_t)tileP * 2 * sizeof(int));
-  c.bits = al((size_t)((tileP * pm + 31) / 32 + 1) * 4);
+  c.bits = al((size_t)tileP * pm + 16);  // crossover choice, 1 byte per gene
   c.vec = al((size_t)3 * m * sizeof(S));
   c.ps = psm ? al((size_t)c.pmS * (c.pmS + 2) * sizeof(double)) : 0;
   c.gv = al((size_t)2 * c.pmS * sizeof(double));

@@ -75,6 +75,30 @@ __device__ __forceinline__ double normal_bm<double>(uint32_t a, uint32_t b) {
   return sqrt(-2.0 * log(u1)) * c;
 }
 
+// two standard normals (cos and sin branches of one Box-Muller transform)
+template <typename S>
+__device__ __forceinline__ void normal_pair(uint32_t a, uint32_t b, S& n0, S& n1);
+template <>
+__device__ __forceinline__ void normal_pair<float>(uint32_t a, uint32_t b, float& n0, float& n1) {
+  const float u1 = ((float)(a >> 8) + 1.0f) * 0x1.0p-24f;  // (0, 1]
+  const float th = ((float)(b >> 8) * 0x1.0p-23f - 1.0f) * 3.14159265358979f;  // [-pi, pi)
+  const float r = sqrtf(-2.0f * __logf(u1));
+  float sn, cs;
+  __sincosf(th, &sn, &cs);
+  n0 = -r * cs;  // cos(th + pi)
+  n1 = -r * sn;  // sin(th + pi)
+}
+template <>
+__device__ __forceinline__ void normal_pair<double>(uint32_t a, uint32_t b, double& n0, double& n1) {
+  const double u1 = ((double)a + 1.0) * 0x1.0p-32;
+  const double u2 = (double)b * 0x1.0p-32;
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  const double r = sqrt(-2.0 * log(u1));
+  n0 = r * cs;
+  n1 = r * sn;
+}
+
 // ---------------------------------------------------------------------------
 // Orderable keys: the reference selects with a stable argsort of FP64 costs
 // (K/empc.py:185) and picks argmin (K/empc.py:234).  Encoding (cost, index)

@@ -31,7 +31,7 @@ struct StageLayout {
 struct RunParams {
   uint64_t seed;
   int64_t gen0;
-  uint64_t thr_cross;  // crossover_prob * 2^32 (Bernoulli by u32 < thr)
+  uint64_t thr_cross;  // crossover_prob * 2^16 (Bernoulli by a 16-bit uniform < thr)
   uint64_t thr_mut;
 };
 
@@ -122,7 +122,7 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.g = al((size_t)(p * p + 2) * sizeof(S));
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
-  s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S) + (size_t)((tileP * p * m + 31) / 32 + 1) * 4);
+  s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S) + (size_t)tileP * p * m + 16);
   s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv + s.bs;
   return s;
 }
@@ -142,12 +142,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // (phase 1b).  Returns false when the CTA has no candidates.
 template <typename S>
 __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, int tile0, int cnt, int tileP, int tPS,
-                                           S* UsT, int* src, uint32_t* tbits, const S* cumin, const S* cumax,
+                                           S* UsT, int* src, uint8_t* tbits, const S* cumin, const S* cumax,
                                            const S* csig, size_t pop_base) {
   const Dims& d = a.d;
   const int m = d.m, pm = d.pm;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
   const double* __restrict__ X = a.state + (size_t)inst * a.SL.sstride;
   const StageLayout& SL = a.SL;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
@@ -175,31 +174,42 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
       }
     }
     if (philox_breed || a.mode == kInitPhilox) {
-      // crossover bit + mutation offset (K/empc.py:197-199), or the uniform
-      // initial knot (K/empc.py:170), per gene into UsT; unrolled so several
-      // independent Philox chains are in flight per thread
-#pragma unroll 4
-      for (int e0 = 0; e0 < tileP * pm; e0 += nthr) {
-        const int e = e0 + tid;
-        const int c = e / pm, g = e - (e / pm) * pm;
-        bool take = false;
-        if (e < tileP * pm && c < cnt) {
-          const int l = g % m;
-          const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
-          if (philox_breed) {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, gen}, key0, key1);
-            take = (uint64_t)r.x < rp.thr_cross;
-            const bool mut = (uint64_t)r.y < rp.thr_mut;
-            UsT[g * tPS + c] = mut ? normal_bm<S>(r.z, r.w) * csig[l] : S(0);
-          } else {
-            const U4 r = philox4x32_10(U4{(uint32_t)g, cand, (uint32_t)inst, kInitTag}, key0, key1);
-            const S lo = cumin[l], hi = cumax[l];
-            const S v = lo + (hi - lo) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
-            UsT[g * tPS + c] = v > hi ? hi : v;
+      // One Philox4x32-10 per PAIR of genes (2q, 2q+1) of a child (counter
+      // (q, child, instance, generation)): 16-bit crossover and mutation
+      // uniforms from words x and y (K/empc.py:197-198), a Box-Muller pair
+      // from z, w for the two mutation offsets (K/empc.py:199); or the two
+      // uniform initial knots from (x, y) and (z, w) (K/empc.py:170)
+      const int hp = (pm + 1) >> 1;
+      const uint32_t tc = (uint32_t)rp.thr_cross, tm = (uint32_t)rp.thr_mut;
+#pragma unroll 2
+      for (int e = tid; e < cnt * hp; e += nthr) {
+        const int c = e / hp, q = e - (e / hp) * hp;
+        const int g0 = 2 * q, g1 = g0 + 1;
+        const bool two = g1 < pm;
+        const int l0 = g0 % m;
+        const int l1 = (l0 + 1 == m) ? 0 : l0 + 1;
+        const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
+        if (philox_breed) {
+          const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, gen}, key0, key1);
+          S n0, n1;
+          normal_pair<S>(r.z, r.w, n0, n1);
+          tbits[c * pm + g0] = (r.x & 0xFFFFu) < tc;
+          UsT[g0 * tPS + c] = (r.y & 0xFFFFu) < tm ? n0 * csig[l0] : S(0);
+          if (two) {
+            tbits[c * pm + g1] = (r.x >> 16) < tc;
+            UsT[g1 * tPS + c] = (r.y >> 16) < tm ? n1 * csig[l1] : S(0);
+          }
+        } else {
+          const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, kInitTag}, key0, key1);
+          const S lo0 = cumin[l0], hi0 = cumax[l0];
+          const S v0 = lo0 + (hi0 - lo0) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
+          UsT[g0 * tPS + c] = v0 > hi0 ? hi0 : v0;
+          if (two) {
+            const S lo1 = cumin[l1], hi1 = cumax[l1];
+            const S v1 = lo1 + (hi1 - lo1) * uniform01<S>(r.z, r.w);
+            UsT[g1 * tPS + c] = v1 > hi1 ? hi1 : v1;
           }
         }
-        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, take);
-        if (lane == 0 && e0 + warp * 32 < tileP * pm) tbits[(e0 + warp * 32) >> 5] = bits;
       }
     }
   }
@@ -237,7 +247,7 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
     for (int e = tid; e < cnt * pm; e += nthr) {
       const int c = e / pm, g = e - (e / pm) * pm;
       const int l = g % m;
-      const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
+      const bool take = tbits[e] != 0;
       const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
       const S lo = cumin[l], hi = cumax[l];
       S v = par + UsT[g * tPS + c];
@@ -265,7 +275,7 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
         v = a.inj_init[((size_t)inst * a.nc + cand) * pm + g];
       } else if (philox_breed) {
         // crossover, mutation, clip (K/empc.py:201-204)
-        const bool take = (tbits[e >> 5] >> (e & 31)) & 1u;
+        const bool take = tbits[e] != 0;
         const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
         const S lo = cumin[l], hi = cumax[l];
         v = par + UsT[g * tPS + c];
@@ -420,7 +430,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     if (lane == 0) cw_[i] += acc;
   }
   EMPC_MARK(8)
-  uint32_t* tbits = reinterpret_cast<uint32_t*>(cw_ + 4 * NP + 5 * m);  // crossover bits, 1 per gene
+  uint8_t* tbits = reinterpret_cast<uint8_t*>(cw_ + 4 * NP + 5 * m);  // crossover choice, 1 byte per gene
   if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
   __syncthreads();
   EMPC_MARK(3)

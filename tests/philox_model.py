@@ -1,6 +1,6 @@
 """numpy model of the in-kernel random streams (the production RNG contract,
 see DESIGN.md): Philox4x32-10 keyed by the 64-bit seed with counters
-(gene, child, instance, generation) for crossover / mutation / noise and
+(gene pair, child, instance, generation) for crossover / mutation / noise and
 (0xFFFFFFFF, child, instance, generation) for the two parent ranks."""
 import numpy as np
 
@@ -23,18 +23,24 @@ def philox(c0, c1, c2, c3, k0, k1):
 
 
 def breed_draws(seed, generation, nc, pm, K, crossover_prob, mutation_prob, instance=0):
-    """parents (nc, 2) ranks, take (nc, pm), mutate (nc, pm), z (nc, pm) standard normals."""
+    """parents (nc, 2) ranks, take (nc, pm), mutate (nc, pm), z (nc, pm) standard normals.
+
+    One Philox call per gene pair (2q, 2q+1) with counter (q, child, instance,
+    generation): 16-bit crossover / mutation uniforms from x / y (low half
+    for gene 2q, high half for 2q+1), Box-Muller cos / sin pair from z, w."""
     k0, k1 = seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF
     child = np.arange(nc)
     x, y, _, _ = philox(0xFFFFFFFF, child, instance, generation, k0, k1)
     parents = np.stack([(x * np.uint64(K)) >> S32, (y * np.uint64(K)) >> S32], axis=1).astype(np.int64)
     g, c = np.meshgrid(np.arange(pm), child, indexing="xy")
-    x, y, z, w = philox(g, c, instance, generation, k0, k1)
-    thr_c = np.uint64(round(crossover_prob * 2.0**32))
-    thr_m = np.uint64(round(mutation_prob * 2.0**32))
-    take = x < thr_c
-    mut = y < thr_m
+    x, y, z, w = philox(g // 2, c, instance, generation, k0, k1)
+    shift = (np.uint64(16) * (g % 2).astype(np.uint64))
+    thr_c = np.uint64(round(crossover_prob * 2.0**16))
+    thr_m = np.uint64(round(mutation_prob * 2.0**16))
+    take = ((x >> shift) & np.uint64(0xFFFF)) < thr_c
+    mut = ((y >> shift) & np.uint64(0xFFFF)) < thr_m
     u1 = ((z >> np.uint64(8)).astype(np.float64) + 1.0) * 2.0**-24
     u2 = (w >> np.uint64(8)).astype(np.float64) * 2.0**-24
-    normal = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+    r = np.sqrt(-2.0 * np.log(u1))
+    normal = np.where(g % 2 == 0, r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2))
     return parents, take, mut, normal
