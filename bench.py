@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--variant", type=int, default=-1, help="force a rollout kernel variant")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tensor-cores", default="auto", choices=["auto", "on", "off"],
+                    help="FP32 rollout recursion on the tcgen05 tensor cores (TF32 split precision): auto = where it "
+                         "measured faster (DESIGN.md §4.8)")
     ap.add_argument("--scorer", default="rollout", choices=["rollout", "condensed"],
                     help="rollout (the north-star kernels, default) or the reference's condensed quadratic "
                          "(SURVEY §8 f2; FP64 quadratic form, roofline against the FP64 peak)")
@@ -262,7 +265,7 @@ def run_ours(args):
         return run_population_sharded(args, rank, world)
     w_total, w, specs, x0s, scaling = workload(args, rank, world)
     sched = w.schedule()
-    st = w.settings(scorer=args.scorer)
+    st = w.settings(scorer=args.scorer, tensor_cores=args.tensor_cores)
     # --- device-resident path: the graph-captured cold solve
     if w.instances > 1:
         batch = P.EmpcBatch(specs, sched, st)

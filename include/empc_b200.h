@@ -163,6 +163,11 @@ int empc_num_variants(empc_handle* h, int32_t* count);
 int empc_set_variant(empc_handle* h, int32_t variant);
 /* Rollout CTAs per SM for the launch plan (0 restores the heuristic). */
 int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm);
+/* Tensor-core rollout (tcgen05, TF32 split precision, FP32 populations with a
+ * diagonal Q): -1 = auto (default: where it measured faster than the FFMA
+ * recursion), 0 = off, 1 = on.  Same function as the FFMA rollout
+ * (K/empc.py:85-119); see DESIGN.md §4.8. */
+int empc_set_tensor_cores(empc_handle* h, int32_t mode);
 
 /* Population sharding over GPUs (K/empc.py:174-208 split
  * across ranks).  A rank holds the K elites (replicated) and the children of

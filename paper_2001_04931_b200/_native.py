@@ -25,7 +25,7 @@ EXPORTS = (
     "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_scorer", "empc_set_problems",
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
-    "empc_set_variant", "empc_set_occupancy", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
+    "empc_set_variant", "empc_set_occupancy", "empc_set_tensor_cores", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
     "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read",
     "empc_plant_linearize_discretize", "empc_plant_integrate", "empc_plant_last_error",
 )
@@ -112,6 +112,7 @@ def load(path: str | None = None):
         "empc_num_variants": (C.c_int, [P, C.POINTER(I32)]),
         "empc_set_variant": (C.c_int, [P, I32]),
         "empc_set_occupancy": (C.c_int, [P, I32]),
+        "empc_set_tensor_cores": (C.c_int, [P, I32]),
         "empc_philox": (C.c_int, [P, P, I32, P]),
         "empc_shard_setup": (C.c_int, [P, I64, I32, I64, I32, I32]),
         "empc_shard_entry_bytes": (C.c_int, [P, C.POINTER(I64)]),
@@ -199,6 +200,9 @@ class Handle:
 
     def set_occupancy(self, ctas_per_sm: int):
         self.call("empc_set_occupancy", int(ctas_per_sm))
+
+    def set_tensor_cores(self, mode: int):
+        self.call("empc_set_tensor_cores", int(mode))
 
 
 def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:

@@ -23,6 +23,7 @@
 #include "empc_kernels.cuh"
 #include "empc_cond.h"
 #include "empc_variants.h"
+#include "empc_tc_rollout.cuh"
 
 using namespace empc;
 
@@ -81,6 +82,7 @@ class EngineBase {
   virtual int num_variants() = 0;
   virtual void set_variant(int) = 0;
   virtual void set_occupancy(int) = 0;
+  virtual void set_tensor_cores(int) = 0;
   virtual void shard_setup(long long, int, long long, int, int) = 0;
   virtual size_t shard_entry_size() = 0;
   virtual void shard_init(const empc_run_args&) = 0;
@@ -391,6 +393,15 @@ class Engine final : public EngineBase {
   }
 
   Launch plan(const Variant<S>& v, int nc, int cps_override = 0) const {
+    if (v.tc) {  // tensor-core rollout: one MMA tile (128 candidates) per CTA
+      Launch L{};
+      L.tile = kTcTile; L.tileP = kTcTile;
+      L.tiles = std::max(1, (nc + kTcTile - 1) / kTcTile);
+      L.threads = kTcTile * v.RR;
+      L.smem = tc_smem(v.tc_nn, v.tc_nk, v.NP, d_.m, d_.T, d_.p, v.RR).total;
+      if (L.smem > (size_t)kMaxSmem) throw InvalidArg{"problem too large for the rollout kernel (" + std::string(v.name) + ")"};
+      return L;
+    }
     const int NRG = v.NP / v.RR;
     const int CC = v.CC;
     auto threads_for = [&](int tileP) {
@@ -443,9 +454,13 @@ class Engine final : public EngineBase {
     if (forced_ >= 0) return variants_.at(forced_);
     auto find = [&](int RR, int CC, bool areg, int ks) -> const Variant<S>* {
       for (auto& v : variants_)
-        if (v.RR == RR && v.CC == CC && v.areg == areg && v.ks == ks && v.dq == dense_) return &v;
+        if (!v.tc && v.RR == RR && v.CC == CC && v.areg == areg && v.ks == ks && v.dq == dense_) return &v;
       return nullptr;
     };
+    if (use_tc()) {
+      for (auto& v : variants_)
+        if (v.tc) return v;
+    }
     if (!dense_ && sizeof(S) == 4) {
       const Variant<S>* pref[4] = {nullptr, nullptr, nullptr, nullptr};
       if (d_.NP <= 8) {
@@ -467,10 +482,22 @@ class Engine final : public EngineBase {
         if (v) return *v;
     }
     for (auto& v : variants_)
-      if (v.dq == dense_ && (dense_ || v.areg)) return v;
+      if (!v.tc && v.dq == dense_ && (dense_ || v.areg)) return v;
     for (auto& v : variants_)
-      if (v.dq == dense_) return v;
+      if (!v.tc && v.dq == dense_) return v;
     return variants_.front();
+  }
+
+  // Tensor-core rollout (rollout_tc_kernel): FP32, diagonal Q.  tc_mode_ 1
+  // forces it, 0 disables it, -1 (default) uses it where it measured faster
+  // than the FFMA recursion on B200 (profiles/)
+  bool use_tc() const {
+    if (sizeof(S) != 4 || dense_ || tc_mode_ == 0) return false;
+    bool have = false;
+    for (auto& v : variants_) have = have || v.tc;
+    if (!have) return false;
+    if (tc_mode_ == 1) return true;
+    return d_.NP >= 64;
   }
 
   void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,
@@ -569,6 +596,7 @@ class Engine final : public EngineBase {
         (d_.NP < 24 && forced_ < 0))
       return false;
     const Variant<S>& v = pick();
+    if (v.tc) return false;
     const PersistVariant<S>* pv = nullptr;
     for (auto& p : persist_)
       if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws) pv = &p;
@@ -734,9 +762,9 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
   }
 
-  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int>;
   GKey gkey(const empc_run_args& r, bool io) const {
-    return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io);
+    return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_);
   }
 
   // One graph per run shape.  io = true also captures the staging H2D copies
@@ -936,6 +964,15 @@ class Engine final : public EngineBase {
         std::fprintf(stderr, " %s=%.2f", names[q], mean);
       }
       std::fprintf(stderr, "\n");
+      if (pick().tc) {  // tensor-core rollout built with -DEMPC_TC_PROF: cycles per step of thread 0
+        double acc[5] = {0, 0, 0, 0, 0};
+        const int slot[5] = {7, 8, 11, 12, 13};
+        for (int c = 0; c < dbg_ctas_; ++c)
+          for (int q = 0; q < 5; ++q) acc[q] += (double)t[(size_t)c * 16 + slot[q]] / dbg_ctas_ / d_.T;
+        std::fprintf(stderr, "tc step (cycles, thread 0): issue=%.0f drive+wait=%.0f math=%.0f store=%.0f bar=%.0f\n",
+                     acc[0], acc[1], acc[2], acc[3], acc[4]);
+        dbg_ctas_ = 0;
+      }
       // persistent kernel: the last generation's selection (marks 13-15)
       double w1 = 0, w2 = 0, w3 = 0;
       int cnt = 0;
@@ -1076,6 +1113,10 @@ class Engine final : public EngineBase {
     if (cps < 0 || cps > 32) throw InvalidArg{"ctas_per_sm must lie in [0, 32]"};
     cps_ = cps;
   }
+  void set_tensor_cores(int mode) override {
+    if (mode < -1 || mode > 1) throw InvalidArg{"tensor_cores must be -1 (auto), 0 (off) or 1 (on)"};
+    tc_mode_ = mode;
+  }
   void set_variant(int v) override {
     if (v >= (int)variants_.size()) throw InvalidArg{"variant out of range"};
     if (v >= 0 && variants_[v].dq != dense_) throw InvalidArg{"variant does not match the Q structure"};
@@ -1131,6 +1172,7 @@ class Engine final : public EngineBase {
   std::vector<Variant<S>> variants_;
   int forced_ = -1;
   int cps_ = 0;  // CTAs per SM for the rollout (0: heuristic)
+  int tc_mode_ = -1;  // tensor-core rollout: -1 auto, 0 off, 1 on
   int cand_base_ = 0;  // global index of local candidate 0 (population sharding)
   bool elites_copied_ = false;  // the last selection also carried the elites over
   long long sh_child_base_ = 0, sh_init_base_ = 0;
@@ -1309,6 +1351,7 @@ int empc_num_variants(empc_handle* h, int32_t* count) {
 int empc_set_variant(empc_handle* h, int32_t variant) { GUARD(h, h->eng->set_variant(variant)); }
 
 int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm) { GUARD(h, h->eng->set_occupancy(ctas_per_sm)); }
+int empc_set_tensor_cores(empc_handle* h, int32_t mode) { GUARD(h, h->eng->set_tensor_cores(mode)); }
 
 int empc_shard_setup(empc_handle* h, int64_t child_base, int32_t n_children, int64_t init_base, int32_t n_init,
                      int32_t owns_elites) {

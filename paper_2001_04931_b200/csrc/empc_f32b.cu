@@ -8,8 +8,7 @@ namespace empc {
 
 std::vector<Variant<float>> variants_f32_small(int NP);
 
-template <>
-std::vector<Variant<float>> variants_for<float>(int NP) {
+static std::vector<Variant<float>> variants_f32_ffma(int NP) {
   switch (NP) {
     case 32: return {FSMALL(32), RVK(float, 32, 2, 2, true, false, 2), RVK(float, 32, 1, 4, true, false, 2)};
     case 48: return {FSMALL(48), RVK(float, 48, 2, 2, true, false, 2), RVK(float, 48, 2, 4, true, false, 2),
@@ -24,6 +23,13 @@ std::vector<Variant<float>> variants_for<float>(int NP) {
     case 128: return {RV(float, 128, 4, 4, false, false), RV(float, 128, 4, 8, false, false), RV(float, 128, 4, 4, false, true)};
   }
   return variants_f32_small(NP);
+}
+
+template <>
+std::vector<Variant<float>> variants_for<float>(int NP) {
+  std::vector<Variant<float>> v = variants_f32_ffma(NP);
+  for (auto& t : variants_f32_tc(NP)) v.push_back(t);
+  return v;
 }
 
 }  // namespace empc

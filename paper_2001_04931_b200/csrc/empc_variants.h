@@ -17,6 +17,9 @@ struct Variant {
   int maxt;
   void (*kernel)(const RolloutArgs<S>);
   const char* name;
+  // tensor-core rollout (rollout_tc_kernel): RR = column groups WG, CC =
+  // state coordinates per thread NH, MMA N / K extents
+  int tc = 0, tc_nn = 0, tc_nk = 0;
 };
 
 // register budget per variant: registers ~ A-in-register rows + accumulators
@@ -37,6 +40,9 @@ constexpr int maxt_for(int NP, int RR, int CC, bool areg, int elem, int KS) {
 
 template <typename S>
 std::vector<Variant<S>> variants_for(int NP);
+
+// FP32 tensor-core rollout variants (empc_f32tc.cu)
+std::vector<Variant<float>> variants_f32_tc(int NP);
 
 template <typename S>
 struct PersistVariant {

@@ -84,9 +84,10 @@ class PopulationShard:
         pa = _problem_arrays(spec)
         arrs = [nat.f64(pa[k]) for k in ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")]
         self.h.call("empc_set_problems", 0, 1, *[nat.dptr(x) for x in arrs])
-        from .empc import _scorer_code
+        from .empc import TC_MODES, _scorer_code
 
         self.h.call("empc_set_scorer", _scorer_code(getattr(settings, "scorer", "rollout"), spec))
+        self.h.set_tensor_cores(TC_MODES[getattr(settings, "tensor_cores", "auto")])
         self.h.call("empc_shard_setup", self.cb, self.cn, self.ib, self.inn, 1 if rank == 0 else 0)
         eb = C.c_int64()
         self.h.call("empc_shard_entry_bytes", C.byref(eb))

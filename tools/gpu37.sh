@@ -1,0 +1,5 @@
+for c in c4 c5 c3; do
+  EMPC_PHASES=1 timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --tensor-cores on > gpurun_out/tcp_${c}.json 2> gpurun_out/tcp_${c}.err
+  grep -E "tc step" gpurun_out/tcp_${c}.err | tail -1
+  python -c "import json;d=json.load(open('gpurun_out/tcp_${c}.json'));print('$c', d['ms_per_step'], d['roofline']['rollout_ms_per_launch'])"
+done
