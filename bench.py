@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import statistics
 import subprocess
@@ -361,11 +362,31 @@ def run_ours(args):
         if condensed:
             peak = pk.get("fp64_tflops", peak)
             peak_src = pk.get("fp64_source", peak_src)
+    desc = ctx.h.describe()
+    tc = re.search(r"tcgen05 tf32x3 N(\d+) K(\d+)", desc) if not condensed else None
+    fp32_equiv = None
+    if tc:
+        # tensor-core rollout: executed TF32 tensor FLOP (3 split terms, padded
+        # N / K, 128-candidate tiles) against the measured dense TF32 peak; the
+        # algorithmic FP32 rate is reported beside it against the FFMA peak
+        NN, NK = int(tc.group(1)), int(tc.group(2))
+        tiles = w.instances * (-(-w.N // 128) + (w.G - 1) * -(-(w.N - w.K) // 128))
+        tensor_flop = tiles * w.T * 3 * 2 * 128 * NN * NK / max(nroll, 1)
+        fp32_equiv = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                      "note": "algorithmic FP32 work (2Tn^2 + 2pnm per candidate) / rollout time vs the FFMA peak"}
+        achieved = tensor_flop / (rollout_ms * 1e-3) / 1e12
+        flop_per_launch = tensor_flop
+        peak, peak_src = 821.7, "half of MEASURED_PEAKS.json bf16_tflops (TF32 MMA: same cycles, half the MACs)"
+        if os.path.exists(FP32_PEAK_FILE):
+            with open(FP32_PEAK_FILE) as f:
+                pk = json.load(f)
+            if "tf32_tflops" in pk:
+                peak, peak_src = pk["tf32_tflops"], pk.get("tf32_source", peak_src)
     traffic = None
     if os.path.exists(TRAFFIC_FILE) and not condensed:
         with open(TRAFFIC_FILE) as f:
             tr = json.load(f)
-        traffic = tr.get(args.config)
+        traffic = tr.get(args.config + ("_tc" if tc else ""))
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -377,11 +398,13 @@ def run_ours(args):
                    "kernel_variant": ctx.h.describe()},
         "latency_ms": {"median": statistics.median(ms_each), "q1": float(np.percentile(ms_each, 25)),
                        "q3": float(np.percentile(ms_each, 75)), "min": min(ms_each)},
-        "roofline": {"bound": "fp64_fma" if condensed else "fp32_fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+        "roofline": {"bound": "fp64_fma" if condensed else "tensor" if tc else "fp32_fma", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "kernel": "cond_score_kernel (breed + FP64 quadratic form)" if condensed else
+                     "rollout_tc_kernel (tcgen05 kind::tf32, 3 split terms; breed + recursion + cost)" if tc else
                      "persist_kernel (whole solve in one cooperative launch: rollouts + selection)"
-                     if "persistent" in ctx.h.describe() else "rollout_kernel",
+                     if "persistent" in desc else "rollout_kernel",
+                     "fp32_equivalent": fp32_equiv,
                      "rollout_ms_per_launch": rollout_ms, "rollout_launches_per_step": nroll,
                      "flop_per_launch": flop_per_launch, "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

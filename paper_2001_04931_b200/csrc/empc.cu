@@ -497,7 +497,11 @@ class Engine final : public EngineBase {
     for (auto& v : variants_) have = have || v.tc;
     if (!have) return false;
     if (tc_mode_ == 1) return true;
-    return d_.NP >= 64;
+    // measured on B200 (profiles/): the tensor-core rollout wins for large
+    // states and for batches that fill the GPU with 128-candidate tiles; the
+    // FFMA kernels (persistent for single problems) win for small single problems
+    const long long tiles = (long long)I_ * ((d_.N - d_.K + kTcTile - 1) / kTcTile);
+    return d_.NP >= 64 || (d_.NP >= 24 && tiles >= 2LL * sms_);
   }
 
   void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 #pragma unroll
     for (int i = 0; i < NH; ++i) hs[i] = hs[i] + cw_[r0 + i] - g[i];
   }
-  __syncthreads();  // UsT and the breeding scratch are consumed
+  __syncthreads();  // the breeding scratch is consumed (UsT stays: knot changes)
 
   // ---- phase 3: Delta hi / lo -> smem (B operand), E_0 = e_0 (all
   // candidates) -> TMEM (A operand)
@@ -261,10 +261,6 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   const uint32_t tA0 = tmem + NN, tA1 = tmem + NN + NK;
   const uint64_t dB0 = tc::sdesc(tc::smem_u32(Dhi), NN * 16, 128);
   const uint64_t dB1 = tc::sdesc(tc::smem_u32(Dlo), NN * 16, 128);
-  // candidate knots for drive updates at knot changes (rows written by the
-  // prologue of this CTA, or the scored population)
-  const S* urow = (c < cnt) ? ((a.mode == kScore ? a.pop_in : a.pop_out) + (pop_base + a.row0 + tile0 + c) * pm)
-                            : nullptr;
 
   // ---- phase 4: horizon recursion, state cost fused (K/empc.py:110-118)
   // (built with -DEMPC_TC_PROF and run with EMPC_PHASES: thread 0
@@ -305,13 +301,14 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
         g[i] = next ? g[i] + hs[i] : cw_[r0 + i];
         hs[i] = S(0);
       }
-      if (urow != nullptr) {
+      {
+        // the knots stay in UsT[gene][cand] (smem) for the whole recursion
         if (!next) {  // rare: the pair jumped (p > T), g = w' + B U_i1
 #pragma unroll 1
           for (int l = 0; l < mP; l += 4) {
             float u[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) u[q] = l + q < m ? urow[i1 * m + l + q] : S(0);
+            for (int q = 0; q < 4; ++q) u[q] = l + q < m ? UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
 #pragma unroll
             for (int i = 0; i < NH; ++i) {
               const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
@@ -323,7 +320,8 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
         for (int l = 0; l < mP; l += 4) {
           float du[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) du[q] = l + q < m ? urow[i2 * m + l + q] - urow[i1 * m + l + q] : S(0);
+          for (int q = 0; q < 4; ++q)
+            du[q] = l + q < m ? UsT[(i2 * m + l + q) * kTcTile + c] - UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
 #pragma unroll
           for (int i = 0; i < NH; ++i) {
             const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
