@@ -14,9 +14,9 @@ std::vector<Variant<float>> variants_f32_tc(int NP) {
   switch (NP) {
     case 4: return {TCV(4, 16, 8, 4, 1, 4)};
     case 8: return {TCV(8, 16, 8, 8, 1, 4)};
-    case 12: return {TCV(12, 16, 16, 12, 1, 4)};
-    case 16: return {TCV(16, 16, 16, 8, 2, 3)};
-    case 24: return {TCV(24, 32, 24, 12, 2, 3)};
+    case 12: return {TCV(12, 16, 16, 12, 1, 5)};
+    case 16: return {TCV(16, 16, 16, 16, 1, 4)};
+    case 24: return {TCV(24, 32, 24, 24, 1, 4), TCV(24, 32, 24, 12, 2, 3)};
     case 32: return {TCV(32, 32, 32, 16, 2, 2)};
     case 48: return {TCV(48, 48, 48, 24, 2, 1)};
     case 64: return {TCV(64, 64, 64, 16, 4, 1)};

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   extern __shared__ __align__(16) unsigned char smem_tc[];
   const Dims& d = a.d;
   const StageLayout& SL = a.SL;
-  const int n = d.n, m = d.m, T = d.T, p = d.p, pm = d.pm;
+  const int n = d.n, m = d.m, T = d.T, p = d.p;
   const int mP = (m + 3) & ~3;  // padded row stride of Bs
   const int inst = blockIdx.y;
   const int tile0 = blockIdx.x * kTcTile;
@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   S* red = reinterpret_cast<S*>(ptr); ptr += sp.red;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(ptr);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(ptr + 8);
+  uint32_t* kmask = reinterpret_cast<uint32_t*>(ptr + 12);  // K-steps (8 columns) where Delta is nonzero
   S* UsT = R1;                                   // [gene][128]
   int* src = reinterpret_cast<int*>(R2);         // breeding scratch ...
   uint8_t* tbits = R2 + 2 * kTcTile * 4;
@@ -155,11 +156,14 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     if (tid == 32) {
       tc::mbar_init(mbar, 1);
       tc::mbar_fence_init();
+      *kmask = 0u;
     }
   }
+  EMPC_MARK(7)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  EMPC_MARK(8)
   // ---- phase 1: K5 prologue (draws, PDL wait, elites, children -> UsT + HBM)
   if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kTcTile, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
   __syncthreads();
@@ -168,51 +172,95 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   // ---- phase 2: input cost z'(W'W (x) R)z (K/empc.py:100-101) over the
   // channels l = h (mod WG), and the drive at the first knot pair
   S cst0 = S(0), cst1 = S(0);
-  for (int l = h; l < m; l += WG) {
-    const S ugl = cug[l];
-    for (int t = 0; t < p; ++t) {
-      S gz = S(0);
-      for (int b = 0; b < p; ++b) {
-        S rz;
-        if (a.r_diag) {
-          rz = crd[l] * (UsT[(b * m + l) * kTcTile + c] - ugl);
-        } else {
-          rz = S(0);
-          for (int l2 = 0; l2 < m; ++l2)
-            rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * kTcTile + c] - cug[l2], rz);
-        }
-        gz = fma(sG[t * p + b], rz, gz);
+  if (a.r_diag && p <= 8) {
+    // z_b = U_b,l - u_goal,l in registers; r_l z' G z with G = W'W from smem
+    for (int l = h; l < m; l += WG) {
+      const S ugl = cug[l];
+      S z[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) z[b] = b < p ? UsT[(b * m + l) * kTcTile + c] - ugl : S(0);
+      S v = S(0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (t >= p) break;
+        S gz = S(0);
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (b < p) gz = fma(sG[t * p + b], z[b], gz);
+        v = fma(z[t], gz, v);
       }
-      cst0 = fma(UsT[(t * m + l) * kTcTile + c] - ugl, gz, cst0);
+      cst0 = fma(crd[l], v, cst0);
+    }
+  } else {
+    for (int l = h; l < m; l += WG) {
+      const S ugl = cug[l];
+      for (int t = 0; t < p; ++t) {
+        S gz = S(0);
+        for (int b = 0; b < p; ++b) {
+          S rz;
+          if (a.r_diag) {
+            rz = crd[l] * (UsT[(b * m + l) * kTcTile + c] - ugl);
+          } else {
+            rz = S(0);
+            for (int l2 = 0; l2 < m; ++l2)
+              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * kTcTile + c] - cug[l2], rz);
+          }
+          gz = fma(sG[t * p + b], rz, gz);
+        }
+        cst0 = fma(UsT[(t * m + l) * kTcTile + c] - ugl, gz, cst0);
+      }
     }
   }
+  EMPC_MARK(11)
   // drive at the knots (K/empc.py:104-105): b_j = w' + B U_j, held as the
-  // segment start g = b_{i1} and slope hs = b_{i2} - b_{i1}
+  // segment start g = b_{i1} and slope hs = b_{i2} - b_{i1}.  seg_drive
+  // adds B U_i1 to g (full) and B (U_i2 - U_i1) to hs, with the knots from
+  // UsT[gene][cand] (smem for the whole recursion) and B rows as float4
   const int r0 = h * NH;  // first state coordinate of this thread
   S g[NH], hs[NH];
-  int ci1 = sI1[0], ci2 = sI2[0];
-  {
+  auto seg_drive = [&](int i1, int i2, bool full) {
+    if (full) {
+#pragma unroll 1
+      for (int l = 0; l < mP; l += 4) {
+        float u[4];
 #pragma unroll
-    for (int i = 0; i < NH; ++i) {
-      g[i] = cw_[r0 + i];
-      hs[i] = S(0);
-    }
-    for (int l = 0; l < m; ++l) {
-      const S u1 = UsT[(ci1 * m + l) * kTcTile + c], u2 = UsT[(ci2 * m + l) * kTcTile + c];
+        for (int q = 0; q < 4; ++q) u[q] = l + q < m ? UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
 #pragma unroll
-      for (int i = 0; i < NH; ++i) {
-        const S b = Bs[(r0 + i) * mP + l];
-        g[i] = fma(b, u1, g[i]);
-        hs[i] = fma(b, u2, hs[i]);
+        for (int i = 0; i < NH; ++i) {
+          const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
+          g[i] = fma(b.x, u[0], fma(b.y, u[1], fma(b.z, u[2], fma(b.w, u[3], g[i]))));
+        }
       }
     }
+#pragma unroll 1
+    for (int l = 0; l < mP; l += 4) {
+      float du[4];
 #pragma unroll
-    for (int i = 0; i < NH; ++i) hs[i] = hs[i] + cw_[r0 + i] - g[i];
+      for (int q = 0; q < 4; ++q)
+        du[q] = l + q < m ? UsT[(i2 * m + l + q) * kTcTile + c] - UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
+#pragma unroll
+      for (int i = 0; i < NH; ++i) {
+        const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
+        hs[i] = fma(b.x, du[0], fma(b.y, du[1], fma(b.z, du[2], fma(b.w, du[3], hs[i]))));
+      }
+    }
+  };
+  int ci1 = sI1[0], ci2 = sI2[0];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    g[i] = cw_[r0 + i];
+    hs[i] = S(0);
   }
+  seg_drive(ci1, ci2, true);
+  EMPC_MARK(12)
   __syncthreads();  // the breeding scratch is consumed (UsT stays: knot changes)
 
   // ---- phase 3: Delta hi / lo -> smem (B operand), E_0 = e_0 (all
   // candidates) -> TMEM (A operand)
+  // Column blocks of Delta that are exactly zero contribute exactly zero:
+  // their K-steps are not issued (e.g. the position columns of a linearized
+  // mechanism without gravity: half of K)
+  uint32_t lmask = 0u;
   for (int e = tid; e < NN * NK; e += nthr) {
     const int i = e / NK, j = e - (e / NK) * NK;
     const S v = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
@@ -220,24 +268,39 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     const int o = (j >> 2) * NN * 4 + i * 4 + (j & 3);
     Dhi[o] = hi;
     Dlo[o] = v - hi;
+    if (v != S(0)) lmask |= 1u << (j >> 3);
   }
+  if (lmask) atomicOr(kmask, lmask);
   S ev[NH];
 #pragma unroll
   for (int i = 0; i < NH; ++i) ev[i] = cx0[r0 + i];
   const uint32_t tmem = *tslot;
   const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)r0;  // my lane, my columns
   // E rows of this thread: its TMEM lane, columns NN + r0 (hi) / NN + NK + r0 (lo)
+  // (the hi part is e itself: kind::tf32 reads the upper 19 bits of each
+  // 32-bit element, which is exactly tf32_trunc(e); lo = e - tf32_trunc(e))
   auto store_e = [&]() {
+    if constexpr (NH % 8 == 0) {
 #pragma unroll
-    for (int q = 0; q < NH / 4; ++q) {
-      float hi[4], lo[4];
+      for (int q = 0; q < NH / 8; ++q) {
+        float lo[8];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        hi[t] = tc::tf32_trunc(ev[4 * q + t]);
-        lo[t] = ev[4 * q + t] - hi[t];
+        for (int t = 0; t < 8; ++t) lo[t] = ev[8 * q + t] - tc::tf32_trunc(ev[8 * q + t]);
+        tc::tmem_st8(tl + NN + 8 * q, ev + 8 * q);
+        tc::tmem_st8(tl + NN + NK + 8 * q, lo);
       }
-      tc::tmem_st4(tl + NN + 4 * q, hi);
-      tc::tmem_st4(tl + NN + NK + 4 * q, lo);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NH / 4; ++q) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          hi[t] = ev[4 * q + t];
+          lo[t] = ev[4 * q + t] - tc::tf32_trunc(ev[4 * q + t]);
+        }
+        tc::tmem_st4(tl + NN + 4 * q, hi);
+        tc::tmem_st4(tl + NN + NK + 4 * q, lo);
+      }
     }
     tc::tmem_wait_st();
   };
@@ -258,6 +321,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   EMPC_MARK(4)
 
   const uint32_t idesc = tc::idesc_tf32(kTcTile, NN);
+  const uint32_t km = *kmask ? *kmask : 1u;  // Delta == 0: one K-step still clears D
   const uint32_t tA0 = tmem + NN, tA1 = tmem + NN + NK;
   const uint64_t dB0 = tc::sdesc(tc::smem_u32(Dhi), NN * 16, 128);
   const uint64_t dB1 = tc::sdesc(tc::smem_u32(Dlo), NN * 16, 128);
@@ -279,13 +343,18 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 #endif
   for (int k = 0; k < T; ++k) {
     if (tid == 0) {
-      // D = E_lo Dhi' + E_hi Dlo' + E_hi Dhi'  (small terms first)
+      // D = E_lo Dhi' + E_hi Dlo' + E_hi Dhi'  (small terms first), over
+      // the nonzero K-steps; the first MMA overwrites D
+      uint32_t acc = 0u;
 #pragma unroll
       for (int s = 0; s < NK / 8; ++s) {
-        const uint64_t ob = (uint64_t)((s * 2 * NN * 16) >> 4);
-        tc::mma_tf32_ts(tmem, tA1 + 8 * s, dB0 + ob, idesc, s > 0);
-        tc::mma_tf32_ts(tmem, tA0 + 8 * s, dB1 + ob, idesc, 1);
-        tc::mma_tf32_ts(tmem, tA0 + 8 * s, dB0 + ob, idesc, 1);
+        if ((km >> s) & 1u) {
+          const uint64_t ob = (uint64_t)((s * 2 * NN * 16) >> 4);
+          tc::mma_tf32_ts(tmem, tA1 + 8 * s, dB0 + ob, idesc, acc);
+          tc::mma_tf32_ts(tmem, tA0 + 8 * s, dB1 + ob, idesc, 1);
+          tc::mma_tf32_ts(tmem, tA0 + 8 * s, dB0 + ob, idesc, 1);
+          acc = 1u;
+        }
       }
       tc::commit(mbar);
     }
@@ -301,34 +370,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
         g[i] = next ? g[i] + hs[i] : cw_[r0 + i];
         hs[i] = S(0);
       }
-      {
-        // the knots stay in UsT[gene][cand] (smem) for the whole recursion
-        if (!next) {  // rare: the pair jumped (p > T), g = w' + B U_i1
-#pragma unroll 1
-          for (int l = 0; l < mP; l += 4) {
-            float u[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) u[q] = l + q < m ? UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
-#pragma unroll
-            for (int i = 0; i < NH; ++i) {
-              const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
-              g[i] = fma(b.x, u[0], fma(b.y, u[1], fma(b.z, u[2], fma(b.w, u[3], g[i]))));
-            }
-          }
-        }
-#pragma unroll 1
-        for (int l = 0; l < mP; l += 4) {
-          float du[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            du[q] = l + q < m ? UsT[(i2 * m + l + q) * kTcTile + c] - UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
-#pragma unroll
-          for (int i = 0; i < NH; ++i) {
-            const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
-            hs[i] = fma(b.x, du[0], fma(b.y, du[1], fma(b.z, du[2], fma(b.w, du[3], hs[i]))));
-          }
-        }
-      }
+      seg_drive(i1, i2, !next);
       ci1 = i1;
       ci2 = i2;
     }
@@ -339,11 +381,16 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     tc::fence_after();
     TC_LAP(1)
     float dv[NH];
+    if constexpr (NH % 8 == 0) {
 #pragma unroll
-    for (int q = 0; q < NH / 4; ++q) {
-      float t4[4] = {0.f, 0.f, 0.f, 0.f};
-      tc::tmem_ld4(tl + 4 * q, t4);
-      dv[4 * q] = t4[0]; dv[4 * q + 1] = t4[1]; dv[4 * q + 2] = t4[2]; dv[4 * q + 3] = t4[3];
+      for (int q = 0; q < NH / 8; ++q) tc::tmem_ld8(tl + 8 * q, dv + 8 * q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NH / 4; ++q) {
+        float t4[4];
+        tc::tmem_ld4(tl + 4 * q, t4);
+        dv[4 * q] = t4[0]; dv[4 * q + 1] = t4[1]; dv[4 * q + 2] = t4[2]; dv[4 * q + 3] = t4[3];
+      }
     }
     tc::tmem_wait_ld();
 #pragma unroll
