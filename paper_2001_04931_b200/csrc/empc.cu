@@ -16,6 +16,7 @@
 #include <string>
 #include <tuple>
 #include <utility>
+#include <thread>
 #include <vector>
 
 #include "../../include/empc_b200.h"
@@ -316,11 +317,24 @@ class Engine final : public EngineBase {
     const int n = d_.n, m = d_.m;
     const int sizes[9] = {n * n, n * m, n, n * n, m * m, n, m, m, m};
     const int offs[9] = {SL_.ad, SL_.bd, SL_.wd, SL_.q, SL_.r, SL_.xg, SL_.ug, SL_.umin, SL_.umax};
-    for (int a = 0; a < 9; ++a) {
+    for (int a = 0; a < 9; ++a)
       if (!arrs[a]) throw InvalidArg{"null problem array"};
-      for (int i = 0; i < count; ++i)
-        std::memcpy(stage_prob_h_ + (size_t)(first + i) * SL_.stride + offs[a], arrs[a] + (size_t)i * sizes[a],
-                    sizeof(double) * sizes[a]);
+    // interleave the caller's stacked arrays into the pinned staging block;
+    // large batches (C5: ~110 MB) are copied by several host threads
+    auto copy = [&](int i0, int i1) {
+      for (int a = 0; a < 9; ++a)
+        for (int i = i0; i < i1; ++i)
+          std::memcpy(stage_prob_h_ + (size_t)(first + i) * SL_.stride + offs[a], arrs[a] + (size_t)i * sizes[a],
+                      sizeof(double) * sizes[a]);
+    };
+    const size_t bytes = (size_t)count * SL_.stride * sizeof(double);
+    const int nth = bytes < ((size_t)8 << 20) ? 1 : (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    if (nth <= 1) {
+      copy(0, count);
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nth; ++t) pool.emplace_back(copy, (int)((long long)count * t / nth), (int)((long long)count * (t + 1) / nth));
+      for (auto& th : pool) th.join();
     }
     bool rd = true;
     for (int i = 0; i < I_ && rd; ++i) {

@@ -30,6 +30,9 @@
 namespace empc {
 
 constexpr int kTcTile = 128;  // candidates per CTA = MMA M
+// knot tile stride UsT[gene][kUsS]: one spare column so the breeding writes
+// (consecutive genes of one child) fall in different banks
+constexpr int kUsS = kTcTile + 1;
 
 struct TcSmem {
   size_t r1, r2, bs, vec, sched, g, red, bar, total;
@@ -40,7 +43,7 @@ __host__ __device__ inline TcSmem tc_smem(int NN, int NK, int NP, int m, int T, 
   auto al = [](size_t x) { return (x + 127) & ~(size_t)127; };
   const int pm = p * m;
   TcSmem s;
-  s.r1 = al((size_t)pm * kTcTile * 4);
+  s.r1 = al((size_t)pm * kUsS * 4);
   const size_t dl = (size_t)2 * NN * NK * 4, br = (size_t)kTcTile * pm + 16 + (size_t)2 * kTcTile * 4;
   s.r2 = al(dl > br ? dl : br);
   s.bs = al((size_t)NP * ((m + 3) & ~3) * 4);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   tc::fence_after();
   EMPC_MARK(8)
   // ---- phase 1: K5 prologue (draws, PDL wait, elites, children -> UsT + HBM)
-  if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kTcTile, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
+  if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kUsS, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
   __syncthreads();
   EMPC_MARK(3)
 
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       const S ugl = cug[l];
       S z[8];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) z[b] = b < p ? UsT[(b * m + l) * kTcTile + c] - ugl : S(0);
+      for (int b = 0; b < 8; ++b) z[b] = b < p ? UsT[(b * m + l) * kUsS + c] - ugl : S(0);
       S v = S(0);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -199,15 +202,15 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
         for (int b = 0; b < p; ++b) {
           S rz;
           if (a.r_diag) {
-            rz = crd[l] * (UsT[(b * m + l) * kTcTile + c] - ugl);
+            rz = crd[l] * (UsT[(b * m + l) * kUsS + c] - ugl);
           } else {
             rz = S(0);
             for (int l2 = 0; l2 < m; ++l2)
-              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * kTcTile + c] - cug[l2], rz);
+              rz = fma((S)P[SL.r + l * m + l2], UsT[(b * m + l2) * kUsS + c] - cug[l2], rz);
           }
           gz = fma(sG[t * p + b], rz, gz);
         }
-        cst0 = fma(UsT[(t * m + l) * kTcTile + c] - ugl, gz, cst0);
+        cst0 = fma(UsT[(t * m + l) * kUsS + c] - ugl, gz, cst0);
       }
     }
   }
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       for (int l = 0; l < mP; l += 4) {
         float u[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) u[q] = l + q < m ? UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
+        for (int q = 0; q < 4; ++q) u[q] = l + q < m ? UsT[(i1 * m + l + q) * kUsS + c] : S(0);
 #pragma unroll
         for (int i = 0; i < NH; ++i) {
           const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       float du[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        du[q] = l + q < m ? UsT[(i2 * m + l + q) * kTcTile + c] - UsT[(i1 * m + l + q) * kTcTile + c] : S(0);
+        du[q] = l + q < m ? UsT[(i2 * m + l + q) * kUsS + c] - UsT[(i1 * m + l + q) * kUsS + c] : S(0);
 #pragma unroll
       for (int i = 0; i < NH; ++i) {
         const float4 b = *reinterpret_cast<const float4*>(Bs + (r0 + i) * mP + l);
