@@ -473,7 +473,7 @@ class Engine final : public EngineBase {
     };
     if (use_tc()) {
       for (auto& v : variants_)
-        if (v.tc) return v;
+        if (v.tc && tc_smem(v.tc_nn, v.tc_nk, v.NP, d_.m, d_.T, d_.p, v.RR).total <= (size_t)kMaxSmem) return v;
     }
     if (!dense_ && sizeof(S) == 4) {
       const Variant<S>* pref[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   uint64_t* mbar = reinterpret_cast<uint64_t*>(ptr);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(ptr + 8);
   uint32_t* kmask = reinterpret_cast<uint32_t*>(ptr + 12);  // K-steps (8 columns) where Delta is nonzero
+  uint64_t* ebar = reinterpret_cast<uint64_t*>(ptr + 16);   // every warp's epilogue of a step is done
   S* UsT = R1;                                   // [gene][128]
   int* src = reinterpret_cast<int*>(R2);         // breeding scratch ...
   uint8_t* tbits = R2 + 2 * kTcTile * 4;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     if (warp == 0) tc::tmem_alloc(tslot, kCols);
     if (tid == 32) {
       tc::mbar_init(mbar, 1);
+      tc::mbar_init(ebar, (uint32_t)nwarps);
       tc::mbar_fence_init();
       *kmask = 0u;
     }
@@ -346,6 +348,11 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 #endif
   for (int k = 0; k < T; ++k) {
     if (tid == 0) {
+      // step k - 1's epilogue is done in every warp (D read, E written)
+      if (k > 0) {
+        tc::mbar_wait(ebar, (uint32_t)((k - 1) & 1));
+        tc::fence_after();
+      }
       // D = E_lo Dhi' + E_hi Dlo' + E_hi Dhi'  (small terms first), over
       // the nonzero K-steps; the first MMA overwrites D
       uint32_t acc = 0u;
@@ -377,10 +384,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       ci1 = i1;
       ci2 = i2;
     }
-    // one warp polls the MMA-completion barrier, the others sleep on a
-    // hardware barrier (polling warps slow the tensor pipe down)
-    if (warp == 0) tc::mbar_wait(mbar, (uint32_t)(k & 1));
-    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    tc::mbar_wait(mbar, (uint32_t)(k & 1));
     tc::fence_after();
     TC_LAP(1)
     float dv[NH];
@@ -412,11 +416,16 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     TC_LAP(2)
     if (k + 1 < T) store_e();
     TC_LAP(3)
+    // no CTA barrier: each warp signals the MMA issuer and runs ahead to the
+    // next step's MMA-completion wait
     tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(ebar)) : "memory");
     TC_LAP(4)
   }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
 #undef TC_LAP
 #ifdef EMPC_TC_PROF
   if (prof) {
