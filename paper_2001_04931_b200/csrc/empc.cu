@@ -59,6 +59,7 @@ int pad_np(int n) {
 struct Launch {
   int tile, tileP, tiles, threads;
   size_t smem;
+  int multi = 0;  // tensor-core rollout: one CTA per instance loops over its tiles
 };
 
 // ---------------------------------------------------------------------------
@@ -413,6 +414,14 @@ class Engine final : public EngineBase {
       L.tiles = std::max(1, (nc + kTcTile - 1) / kTcTile);
       L.threads = kTcTile * v.RR;
       L.smem = tc_smem(v.tc_nn, v.tc_nk, v.NP, d_.m, d_.T, d_.p, v.RR).total;
+      // many instances with several tiles each (C5): one CTA per instance
+      // stages the problem once and loops over the instance's tiles
+      const size_t msm = tc_smem(v.tc_nn, v.tc_nk, v.NP, d_.m, d_.T, d_.p, v.RR, true).total;
+      if (I_ > 1 && L.tiles > 1 && (long long)I_ >= 4LL * sms_ && msm <= (size_t)kMaxSmem && tc_multi_ok_) {
+        L.multi = 1;
+        L.tiles = 1;
+        L.smem = msm;
+      }
       if (L.smem > (size_t)kMaxSmem) throw InvalidArg{"problem too large for the rollout kernel (" + std::string(v.name) + ")"};
       return L;
     }
@@ -543,6 +552,7 @@ class Engine final : public EngineBase {
     a.copy_elites = elites_copied_ ? 0 : 1;
     a.cond = cond_;
     a.cstride = cond_layout(d_.pm).stride;
+    a.tc_multi = L.multi;
     elites_copied_ = false;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
@@ -1191,6 +1201,7 @@ class Engine final : public EngineBase {
   int forced_ = -1;
   int cps_ = 0;  // CTAs per SM for the rollout (0: heuristic)
   int tc_mode_ = -1;  // tensor-core rollout: -1 auto, 0 off, 1 on
+  bool tc_multi_ok_ = std::getenv("EMPC_TC_NO_MULTI") == nullptr;
   int cand_base_ = 0;  // global index of local candidate 0 (population sharding)
   bool elites_copied_ = false;  // the last selection also carried the elites over
   long long sh_child_base_ = 0, sh_init_base_ = 0;

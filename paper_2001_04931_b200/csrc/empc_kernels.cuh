@@ -77,6 +77,7 @@ struct RolloutArgs {
   int qcap;
   const double* cond;       // condensed scorer: per instance P, g, ref, J_ref (empc_cond.h)
   int cstride;              // doubles per instance of `cond`
+  int tc_multi;             // tensor-core rollout: each CTA loops over tiles (Delta staged once per CTA)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -143,7 +144,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 template <typename S>
 __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, int tile0, int cnt, int tileP, int tPS,
                                            S* UsT, int* src, uint8_t* tbits, const S* cumin, const S* cumax,
-                                           const S* csig, size_t pop_base) {
+                                           const S* csig, size_t pop_base, bool elites = true) {
   const Dims& d = a.d;
   const int m = d.m, pm = d.pm;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -220,7 +221,7 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
   EMPC_MARK(2)
   // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
   // population are the sorted elites with their carried costs.
-  if (breed && a.copy_elites) {  // otherwise the selection kernel already did
+  if (breed && a.copy_elites && elites) {  // otherwise the selection kernel already did
     for (int e = blockIdx.x; e < d.K; e += gridDim.x) {
       const int s = a.elite_idx[(size_t)inst * d.K + e];
       const S* from = a.pop_in + (pop_base + s) * pm;

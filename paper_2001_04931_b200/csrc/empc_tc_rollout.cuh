@@ -35,24 +35,27 @@ constexpr int kTcTile = 128;  // candidates per CTA = MMA M
 constexpr int kUsS = kTcTile + 1;
 
 struct TcSmem {
-  size_t r1, r2, bs, vec, sched, g, red, bar, total;
+  size_t r1, r2, r3, bs, vec, sched, g, red, bar, total;
 };
 
 // shared-memory plan of rollout_tc_kernel (host and device agree)
-__host__ __device__ inline TcSmem tc_smem(int NN, int NK, int NP, int m, int T, int p, int WG) {
+// multi: the CTA loops over several tiles, Delta gets its own region (r3)
+// instead of aliasing the breeding scratch (r2)
+__host__ __device__ inline TcSmem tc_smem(int NN, int NK, int NP, int m, int T, int p, int WG, bool multi = false) {
   auto al = [](size_t x) { return (x + 127) & ~(size_t)127; };
   const int pm = p * m;
   TcSmem s;
   s.r1 = al((size_t)pm * kUsS * 4);
   const size_t dl = (size_t)2 * NN * NK * 4, br = (size_t)kTcTile * pm + 16 + (size_t)2 * kTcTile * 4;
-  s.r2 = al(dl > br ? dl : br);
+  s.r2 = al(multi ? br : (dl > br ? dl : br));
+  s.r3 = multi ? al(dl) : 0;
   s.bs = al((size_t)NP * ((m + 3) & ~3) * 4);
   s.vec = al((size_t)(4 * NP + 5 * m) * 4);
   s.sched = al((size_t)T * 12);
   s.g = al((size_t)(p * p + 2) * 4);
   s.red = al((size_t)WG * kTcTile * 4);
   s.bar = 128;  // mbarrier + TMEM address
-  s.total = s.r1 + s.r2 + s.bs + s.vec + s.sched + s.g + s.red + s.bar;
+  s.total = s.r1 + s.r2 + s.r3 + s.bs + s.vec + s.sched + s.g + s.red + s.bar;
   return s;
 }
 
@@ -69,8 +72,10 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   const int n = d.n, m = d.m, T = d.T, p = d.p;
   const int mP = (m + 3) & ~3;  // padded row stride of Bs
   const int inst = blockIdx.y;
-  const int tile0 = blockIdx.x * kTcTile;
-  const int cnt = min(kTcTile, a.nc - tile0);
+  const bool multi = a.tc_multi != 0;
+  const int ntiles = (a.nc + kTcTile - 1) / kTcTile;
+  int tile0 = blockIdx.x * kTcTile;
+  int cnt = min(kTcTile, a.nc - tile0);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
   const int c = tid & (kTcTile - 1);  // candidate = TMEM lane
@@ -80,10 +85,11 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   const size_t pop_base = (size_t)inst * a.rows;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
 
-  const TcSmem sp = tc_smem(NN, NK, NP, m, T, p, WG);
+  const TcSmem sp = tc_smem(NN, NK, NP, m, T, p, WG, multi);
   unsigned char* ptr = smem_tc;
   S* R1 = reinterpret_cast<S*>(ptr); ptr += sp.r1;
   unsigned char* R2 = ptr; ptr += sp.r2;
+  unsigned char* R3 = multi ? ptr : R2; ptr += sp.r3;
   S* Bs = reinterpret_cast<S*>(ptr); ptr += sp.bs;  // [NP][m]
   S* cw_ = reinterpret_cast<S*>(ptr); ptr += sp.vec;
   S* cqd = cw_ + NP;
@@ -106,10 +112,27 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   S* UsT = R1;                                   // [gene][128]
   int* src = reinterpret_cast<int*>(R2);         // breeding scratch ...
   uint8_t* tbits = R2 + 2 * kTcTile * 4;
-  S* Dhi = reinterpret_cast<S*>(R2);             // ... then Delta hi / lo [NK/4][NN][4]
+  S* Dhi = reinterpret_cast<S*>(R3);             // ... then (or beside it) Delta hi / lo [NK/4][NN][4]
   S* Dlo = Dhi + (size_t)NN * NK;
   // TMEM columns: D [0, NN), E_hi [NN, NN + NK), E_lo [NN + NK, NN + 2 NK)
   constexpr uint32_t kCols = tc::tmem_cols_for(NN + 2 * NK);
+
+  // Column blocks of Delta that are exactly zero contribute exactly zero:
+  // their K-steps are not issued (e.g. the position columns of a linearized
+  // mechanism without gravity, SURVEY §8d: half of K)
+  auto stage_delta = [&]() {
+    uint32_t lmask = 0u;
+    for (int e = tid; e < NN * NK; e += nthr) {
+      const int i = e / NK, j = e - (e / NK) * NK;
+      const S v = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
+      const S hi = tc::to_tf32(v);
+      const int o = (j >> 2) * NN * 4 + i * 4 + (j & 3);
+      Dhi[o] = hi;
+      Dlo[o] = v - hi;
+      if (v != S(0)) lmask |= 1u << (j >> 3);
+    }
+    if (lmask) atomicOr(kmask, lmask);
+  };
 
   EMPC_MARK(0)
   // ---- phase 0: problem -> smem (independent of the producer grid)
@@ -168,9 +191,16 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  if (multi && cnt > 0) stage_delta();  // once per CTA (own region); kmask is read after later barriers
   EMPC_MARK(8)
+  const uint32_t tmem = *tslot;
+  int gstep = 0;  // steps of this CTA over all its tiles (mbarrier phases)
+  for (int tile = blockIdx.x, it = 0; it == 0 || tile < ntiles; tile += gridDim.x, ++it) {
+  tile0 = tile * kTcTile;
+  cnt = min(kTcTile, a.nc - tile0);
   // ---- phase 1: K5 prologue (draws, PDL wait, elites, children -> UsT + HBM)
-  if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kUsS, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
+  if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kUsS, UsT, src, tbits, cumin, cumax, csig, pop_base, it == 0))
+    return;  // (only a CTA without any tile gets here: nothing was allocated for it)
   __syncthreads();
   EMPC_MARK(3)
 
@@ -262,24 +292,10 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 
   // ---- phase 3: Delta hi / lo -> smem (B operand), E_0 = e_0 (all
   // candidates) -> TMEM (A operand)
-  // Column blocks of Delta that are exactly zero contribute exactly zero:
-  // their K-steps are not issued (e.g. the position columns of a linearized
-  // mechanism without gravity, SURVEY §8d: half of K)
-  uint32_t lmask = 0u;
-  for (int e = tid; e < NN * NK; e += nthr) {
-    const int i = e / NK, j = e - (e / NK) * NK;
-    const S v = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
-    const S hi = tc::to_tf32(v);
-    const int o = (j >> 2) * NN * 4 + i * 4 + (j & 3);
-    Dhi[o] = hi;
-    Dlo[o] = v - hi;
-    if (v != S(0)) lmask |= 1u << (j >> 3);
-  }
-  if (lmask) atomicOr(kmask, lmask);
+  if (!multi) stage_delta();
   S ev[NH];
 #pragma unroll
   for (int i = 0; i < NH; ++i) ev[i] = cx0[r0 + i];
-  const uint32_t tmem = *tslot;
   const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)r0;  // my lane, my columns
   // E rows of this thread: its TMEM lane, columns NN + r0 (hi) / NN + NK + r0 (lo)
   // (the hi part is e itself: kind::tf32 reads the upper 19 bits of each
@@ -322,7 +338,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  pdl_trigger();
+  if (it == 0) pdl_trigger();
   EMPC_MARK(4)
 
   const uint32_t idesc = tc::idesc_tf32(kTcTile, NN);
@@ -346,11 +362,11 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 #else
 #define TC_LAP(I)
 #endif
-  for (int k = 0; k < T; ++k) {
+  for (int k = 0; k < T; ++k, ++gstep) {
     if (tid == 0) {
-      // step k - 1's epilogue is done in every warp (D read, E written)
-      if (k > 0) {
-        tc::mbar_wait(ebar, (uint32_t)((k - 1) & 1));
+      // the previous step's epilogue is done in every warp (D read, E written)
+      if (gstep > 0) {
+        tc::mbar_wait(ebar, (uint32_t)((gstep - 1) & 1));
         tc::fence_after();
       }
       // D = E_lo Dhi' + E_hi Dlo' + E_hi Dhi'  (small terms first), over
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       ci1 = i1;
       ci2 = i2;
     }
-    tc::mbar_wait(mbar, (uint32_t)(k & 1));
+    tc::mbar_wait(mbar, (uint32_t)(gstep & 1));
     tc::fence_after();
     TC_LAP(1)
     float dv[NH];
@@ -438,7 +454,6 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   }
 #endif
   EMPC_MARK(5)
-  if (warp == 0) tc::tmem_dealloc(tmem, kCols);
 
   // ---- deterministic reduction over the column groups
   red[h * kTcTile + c] = cst0 + cst1;
@@ -467,6 +482,12 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       }
     }
   }
+  __syncthreads();  // red / UsT are reused by the next tile
+  }  // tiles
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_dealloc(tmem, kCols);
   EMPC_MARK(6)
 }
 

@@ -155,3 +155,26 @@ def test_tc_init_generation_equals_ffma_population():
                                                  tensor_cores="off"), x0)
     np.testing.assert_array_equal(a.population.candidates, b.population.candidates)
     np.testing.assert_allclose(a.population.costs, b.population.costs, rtol=RTOL32)
+
+
+def test_tc_multi_tile_ctas_match_ffma_and_oracle():
+    """>= 4 x 148 instances with several tiles each: one CTA per instance
+    loops over its tiles (problem staged once).  Cold start = same Philox
+    population as the FFMA kernel, costs to the FP32 contract; a 3-generation
+    solve's population costs match the oracle."""
+    from paper_2001_04931_b200 import workloads as W
+
+    w = W.Workload("multi", 3, 20, 2, 300, 20, 1, instances=600)
+    specs, x0s = W.build(w)
+    on = P.EmpcBatch(specs, w.schedule(), w.settings(tensor_cores="on"))
+    assert _uses_tc(on.ctx), on.ctx.h.describe()
+    off = P.EmpcBatch(specs, w.schedule(), w.settings(tensor_cores="off"))
+    a, b = on.solve(x0s), off.solve(x0s)
+    np.testing.assert_array_equal(a.population.candidates, b.population.candidates)
+    np.testing.assert_allclose(a.population.costs, b.population.costs, rtol=RTOL32)
+    w3 = W.Workload("multi", 3, 20, 2, 300, 20, 3, instances=600)
+    r = P.EmpcBatch(specs, w3.schedule(), w3.settings(tensor_cores="on")).solve(x0s)
+    for i in (0, 311, 599):
+        pr = O.Problem.from_spec(specs[i])
+        np.testing.assert_allclose(r.population.costs[i], O.rollout_costs(r.population.candidates[i], pr, x0s[i]),
+                                   rtol=RTOL32)
