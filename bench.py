@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(DESCRIPTIONS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--instances", type=int, default=None, help="override the instance count (C5)")
+    ap.add_argument("--num-sims", type=int, default=None,
+                    help="override the population size N (e.g. one rank's share of a sharded C4 population)")
     ap.add_argument("--variant", type=int, default=-1, help="force a rollout kernel variant")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,6 +84,8 @@ def workload(args, rank, world):
     w = W.WORKLOADS[args.config]
     if args.instances is not None:
         w = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=args.instances)
+    if args.num_sims is not None:
+        w = W.Workload(w.name, w.dof, w.T, w.p, args.num_sims, w.K, w.G, instances=w.instances)
     if w.instances > 1:  # shard instances across ranks
         from paper_2001_04931_b200.shard import instance_range
 
@@ -370,7 +374,11 @@ def run_ours(args):
         # N / K, 128-candidate tiles) against the measured dense TF32 peak; the
         # algorithmic FP32 rate is reported beside it against the FFMA peak
         NN, NK = int(tc.group(1)), int(tc.group(2))
-        tiles = w.instances * (-(-w.N // 128) + (w.G - 1) * -(-(w.N - w.K) // 128))
+        def launch_tiles(nc):  # the host's TC launch plan (empc.cu plan()): 128-row MMA tiles
+            if w.instances == 1:
+                return -(-nc // max(1, min(128, -(-nc // 148))))
+            return w.instances * -(-nc // 128)
+        tiles = launch_tiles(w.N) + (w.G - 1) * launch_tiles(w.N - w.K)
         # issued K-steps: 8-column blocks of Delta = Ad - I with a nonzero entry
         # (the kernel skips all-zero blocks; every instance of a workload has
         # the same structure)

@@ -410,8 +410,11 @@ class Engine final : public EngineBase {
   Launch plan(const Variant<S>& v, int nc, int cps_override = 0) const {
     if (v.tc) {  // tensor-core rollout: one MMA tile (128 candidates) per CTA
       Launch L{};
-      L.tile = kTcTile; L.tileP = kTcTile;
-      L.tiles = std::max(1, (nc + kTcTile - 1) / kTcTile);
+      // one instance: spread the candidates over all SMs (rows beyond the
+      // tile's count are MMA padding whose epilogue warps idle)
+      const int tsz = I_ == 1 ? std::max(1, std::min(kTcTile, (nc + sms_ - 1) / sms_)) : kTcTile;
+      L.tile = tsz; L.tileP = kTcTile;
+      L.tiles = std::max(1, (nc + tsz - 1) / tsz);
       L.threads = kTcTile * v.RR;
       L.smem = tc_smem(v.tc_nn, v.tc_nk, v.NP, d_.m, d_.T, d_.p, v.RR).total;
       // many instances with several tiles each (C5): one CTA per instance
@@ -524,7 +527,10 @@ class Engine final : public EngineBase {
     // states and for batches that fill the GPU with 128-candidate tiles; the
     // FFMA kernels (persistent for single problems) win for small single problems
     const long long tiles = (long long)I_ * ((d_.N - d_.K + kTcTile - 1) / kTcTile);
-    return d_.NP >= 64 || (d_.NP >= 24 && tiles >= 2LL * sms_);
+    // (one instance: a tile per SM at any size; below ~16 children per SM --
+    // e.g. one rank's share of C4 over 8 GPUs -- the FFMA kernel is faster)
+    if (I_ == 1) return d_.NP >= 64 && (d_.N - d_.K) >= 16 * sms_;
+    return d_.NP >= 24 && tiles >= 2LL * sms_;
   }
 
   void launch_rollout(int mode, int nc, int row0, int rows, int evolve, const S* pin, const S* cin, S* pout, S* cout,

@@ -73,9 +73,12 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   const int mP = (m + 3) & ~3;  // padded row stride of Bs
   const int inst = blockIdx.y;
   const bool multi = a.tc_multi != 0;
-  const int ntiles = (a.nc + kTcTile - 1) / kTcTile;
-  int tile0 = blockIdx.x * kTcTile;
-  int cnt = min(kTcTile, a.nc - tile0);
+  // candidates per tile a.tile <= 128 (MMA M stays 128; rows >= cnt are
+  // padding): small populations spread over all SMs
+  const int tsz = a.tile;
+  const int ntiles = (a.nc + tsz - 1) / tsz;
+  int tile0 = blockIdx.x * tsz;
+  int cnt = min(tsz, a.nc - tile0);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
   const int c = tid & (kTcTile - 1);  // candidate = TMEM lane
@@ -196,8 +199,11 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   const uint32_t tmem = *tslot;
   int gstep = 0;  // steps of this CTA over all its tiles (mbarrier phases)
   for (int tile = blockIdx.x, it = 0; it == 0 || tile < ntiles; tile += gridDim.x, ++it) {
-  tile0 = tile * kTcTile;
-  cnt = min(kTcTile, a.nc - tile0);
+  tile0 = tile * tsz;
+  cnt = min(tsz, a.nc - tile0);
+  // warps whose 32 TMEM lanes are all padding skip the epilogue (they still
+  // follow the step barriers)
+  const bool wlive = 32 * (warp & 3) < cnt;
   // ---- phase 1: K5 prologue (draws, PDL wait, elites, children -> UsT + HBM)
   if (!breed_tile<S>(a, inst, tile0, cnt, kTcTile, kUsS, UsT, src, tbits, cumin, cumax, csig, pop_base, it == 0))
     return;  // (only a CTA without any tile gets here: nothing was allocated for it)
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   S cst0 = S(0), cst1 = S(0);
   if (a.r_diag && p <= 8) {
     // z_b = U_b,l - u_goal,l in registers; r_l z' G z with G = W'W from smem
-    for (int l = h; l < m; l += WG) {
+    for (int l = wlive ? h : m; l < m; l += WG) {
       const S ugl = cug[l];
       S z[8];
 #pragma unroll
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       cst0 = fma(crd[l], v, cst0);
     }
   } else {
-    for (int l = h; l < m; l += WG) {
+    for (int l = wlive ? h : m; l < m; l += WG) {
       const S ugl = cug[l];
       for (int t = 0; t < p; ++t) {
         S gz = S(0);
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     g[i] = cw_[r0 + i];
     hs[i] = S(0);
   }
-  seg_drive(ci1, ci2, true);
+  if (wlive) seg_drive(ci1, ci2, true);
   EMPC_MARK(12)
   __syncthreads();  // the breeding scratch is consumed (UsT stays: knot changes)
 
@@ -396,13 +402,14 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
         g[i] = next ? g[i] + hs[i] : cw_[r0 + i];
         hs[i] = S(0);
       }
-      seg_drive(i1, i2, !next);
+      if (wlive) seg_drive(i1, i2, !next);
       ci1 = i1;
       ci2 = i2;
     }
     tc::mbar_wait(mbar, (uint32_t)(gstep & 1));
     tc::fence_after();
     TC_LAP(1)
+    if (wlive) {
     float dv[NH];
     if constexpr (NH % 8 == 0) {
 #pragma unroll
@@ -431,6 +438,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     }
     TC_LAP(2)
     if (k + 1 < T) store_e();
+    }
     TC_LAP(3)
     // no CTA barrier: each warp signals the MMA issuer and runs ahead to the
     // next step's MMA-completion wait
