@@ -178,3 +178,22 @@ def test_tc_multi_tile_ctas_match_ffma_and_oracle():
         pr = O.Problem.from_spec(specs[i])
         np.testing.assert_allclose(r.population.costs[i], O.rollout_costs(r.population.candidates[i], pr, x0s[i]),
                                    rtol=RTOL32)
+
+
+def test_tc_population_sharding_matches_unsharded():
+    """C4-style population sharding with the tensor-core rollout on every rank
+    (2 ranks in lock-step on one GPU): the unsharded result bit for bit, since
+    a candidate's arithmetic does not depend on its tile or row."""
+    from paper_2001_04931_b200 import workloads as W
+    from paper_2001_04931_b200.shard import solve_population_emulated
+
+    spec, x0 = W.nlink_problem(32, 30, 0)
+    sched = P.KnotSchedule(30, 3)
+    st = P.EmpcSettings(num_sims=5824, num_parents=1024, generations=3, seed=5)
+    ref = P.solve_empc(spec, sched, st, x0)
+    ctx = P.empc._context(64, 32, 30, 3, 5824, 1024, 1, False, "fp32")
+    assert _uses_tc(ctx), ctx.h.describe()
+    (u, best, cost, row), shards = solve_population_emulated(spec, sched, st, x0, 2)
+    np.testing.assert_array_equal(best, ref.best)
+    np.testing.assert_array_equal(u, ref.u)
+    assert cost == ref.best_cost
