@@ -306,10 +306,14 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
   // E rows of this thread: its TMEM lane, columns NN + r0 (hi) / NN + NK + r0 (lo)
   // (the hi part is e itself: kind::tf32 reads the upper 19 bits of each
   // 32-bit element, which is exactly tf32_trunc(e); lo = e - tf32_trunc(e))
-  auto store_e = [&]() {
+  auto store_e = [&](uint32_t qmask) {  // qmask: 8-column chunks to store (NH % 8 == 0)
     if constexpr (NH % 8 == 0) {
 #pragma unroll
       for (int q = 0; q < NH / 8; ++q) {
+        // per-chunk skipping pays where one thread holds every coordinate
+        // (WG = 1, C5); with several column groups whole threads skip
+        // (e_live below) and the unconditional store schedules better (C4)
+        if (WG == 1 && !((qmask >> q) & 1u)) continue;
         float lo[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) lo[t] = ev[8 * q + t] - tc::tf32_trunc(ev[8 * q + t]);
@@ -331,7 +335,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
     }
     tc::tmem_wait_st();
   };
-  store_e();
+  store_e(~0u);  // (the nonzero K-steps of Delta are known after the next barrier)
   if (h == 0) {  // K padding columns stay zero
     const float z[4] = {0.f, 0.f, 0.f, 0.f};
     for (int kc = (NH * WG) / 4; kc < NK / 4; ++kc) {
@@ -349,6 +353,10 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
 
   const uint32_t idesc = tc::idesc_tf32(kTcTile, NN);
   const uint32_t km = *kmask ? *kmask : 1u;  // Delta == 0: one K-step still clears D
+  // E columns that no issued K-step reads (all-zero blocks of Delta) are not
+  // stored after E_0: e.g. the position coordinates of an N-link arm
+  const uint32_t emask = NH % 8 != 0 ? ~0u : (km >> (r0 / 8)) & ((1u << (NH / 8)) - 1u);
+  const bool e_live = emask != 0u;
   const uint32_t tA0 = tmem + NN, tA1 = tmem + NN + NK;
   const uint64_t dB0 = tc::sdesc(tc::smem_u32(Dhi), NN * 16, 128);
   const uint64_t dB1 = tc::sdesc(tc::smem_u32(Dlo), NN * 16, 128);
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kTcTile * WG, MINB) rollout_tc_kernel(const Ro
       }
     }
     TC_LAP(2)
-    if (k + 1 < T) store_e();
+    if (k + 1 < T && e_live) store_e(emask);
     }
     TC_LAP(3)
     // no CTA barrier: each warp signals the MMA issuer and runs ahead to the
