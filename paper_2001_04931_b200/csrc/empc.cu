@@ -344,6 +344,15 @@ class Engine final : public EngineBase {
         if (e / m != e % m && R[e] != 0.0) { rd = false; break; }
     }
     r_diag_ = rd;
+    // half-K: Delta = Ad - I has no nonzero entry in its left NP / 2 columns
+    bool hk = true;
+    for (int i = 0; i < I_ && hk; ++i) {
+      const double* A = stage_prob_h_ + (size_t)i * SL_.stride + SL_.ad;
+      for (int r = 0; r < n && hk; ++r)
+        for (int c = 0; c < std::min(n, d_.NP / 2); ++c)
+          if (A[r * n + c] - (r == c ? 1.0 : 0.0) != 0.0) { hk = false; break; }
+    }
+    halfk_ = hk;
     have_prob_ = true;
   }
 
@@ -632,8 +641,15 @@ class Engine final : public EngineBase {
     const Variant<S>& v = pick();
     if (v.tc) return false;
     const PersistVariant<S>* pv = nullptr;
+    const bool hk = halfk_ && halfk_ok_;
     for (auto& p : persist_)
-      if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws) pv = &p;
+      if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws &&
+          p.hk == hk)
+        pv = &p;
+    if (!pv && hk)  // no half-K instantiation of this variant: the full matvec
+      for (auto& p : persist_)
+        if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws && !p.hk)
+          pv = &p;
     if (!pv) return false;
     const int nc = d_.N - d_.K;
     const Launch Le = plan(v, nc, 1);
@@ -698,7 +714,7 @@ class Engine final : public EngineBase {
     ++rollout_launches_;
     if (timed) post();
     persist_desc_ = std::string("persistent grid=") + std::to_string(grid) + " threads=" + std::to_string(threads) +
-                    " smem=" + std::to_string(smem);
+                    " smem=" + std::to_string(smem) + (pv->hk ? " halfK" : "");
     return true;
   }
 
@@ -796,9 +812,10 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
   }
 
-  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int, bool>;
   GKey gkey(const empc_run_args& r, bool io) const {
-    return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_);
+    return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_,
+                           halfk_);
   }
 
   // One graph per run shape.  io = true also captures the staging H2D copies
@@ -1240,6 +1257,7 @@ class Engine final : public EngineBase {
   size_t cws_n_ = 0;
   size_t select_smem_ = 0;
   bool have_sched_ = false, have_prob_ = false, r_diag_ = true;
+  bool halfk_ = false, halfk_ok_ = std::getenv("EMPC_NO_HALFK") == nullptr;
   std::vector<Slot> slots_;
   S *scratch_pop_ = nullptr, *scratch_cost_ = nullptr;
   double* scratch_dbl_ = nullptr;

@@ -314,14 +314,19 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
 // (1) wait for the producer, elite carry-over and breeding; (2) B at the
 // knots and the knot-space input cost; (3) the horizon recursion.
 
-template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS>
+// HK: the left half of Delta's columns is exactly zero (the position columns
+// of a linearized mechanism without gravity): the matvec runs over
+// the right half only, split over the lane pair as usual (exact: the skipped
+// products are zeros; the summation order of the rest changes)
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, bool HK = false>
 __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage, size_t persist_scratch) {
   constexpr int NRG = NP / RR;
   constexpr int VEC = Geo<S>::VEC;
   constexpr int NPS = Geo<S>::nps(NP);
   constexpr int NSPLIT = (RR * CC >= 8) ? 1 : ((RR * CC >= 4) ? 2 : 4);
-  constexpr int NJ = NP / VEC / KS;  // 16-byte column groups per reduction half
-  constexpr int NPH = NP / KS;       // columns per reduction half
+  constexpr int NPH = HK ? NP / KS / 2 : NP / KS;  // columns per reduction half
+  constexpr int NJ = NPH / VEC;                    // 16-byte column groups per reduction half
+  static_assert(!HK || (NP / 2) % (KS * VEC) == 0, "half-K split");
   static_assert(!WS || 32 % (NRG * KS) == 0, "warp-synchronous variants need whole candidate groups per warp");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Dims& d = a.d;
@@ -446,7 +451,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   // padding threads shadow candidate group 0 so that every lane of a warp
   // takes part in the shuffles; their results are never stored
   const int c0 = active ? cg * CC : 0;
-  const int jbase = ks * NPH;
+  const int jbase = (HK ? NP / 2 : 0) + ks * NPH;
   // epilogue split: with KS = 2 each lane of the pair finishes half of the
   // candidates (CH of them, starting at candidate ce)
   constexpr int CH = KS == 2 ? CC / 2 : CC;
@@ -1060,14 +1065,14 @@ struct PersistArgs {
   double* out;
 };
 
-template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT>
+template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT, bool HK = false>
 __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   RolloutArgs<S> a = P.ro;
   const int N = a.d.N, K = a.d.K, pm = a.d.pm;
   using OT = typename std::conditional<sizeof(S) == 4, uint32_t, uint64_t>::type;
   const size_t qstride = (size_t)a.qcap * 2 * sizeof(OT);
-  rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(a, true, P.scratch);
+  rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(a, true, P.scratch);
   int cur = 0;
   for (int g = 0; g < P.evolves; ++g) {
     EMPC_MARK(13)
@@ -1092,7 +1097,7 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     b.cost_out = P.cost[cur ^ 1];
     b.qcount = P.incremental ? P.qcount + (g & 1) : nullptr;
     b.qlist = (char*)P.qlist + (g & 1) * qstride;
-    rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS>(b, false, P.scratch);
+    rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(b, false, P.scratch);
     cur ^= 1;
   }
   grid.sync();

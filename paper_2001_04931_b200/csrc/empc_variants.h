@@ -50,6 +50,7 @@ struct PersistVariant {
   bool areg;
   int ks;
   void (*kernel)(const PersistArgs<S>);
+  bool hk = false;  // half-K matvec (left half of Delta's columns zero)
 };
 
 template <typename S>

@@ -510,3 +510,34 @@ def test_population_sharding_matches_unsharded(world):
     # and the union of the children slices is the unsharded children block
     kids = np.concatenate([s.local_population()[0][64:] for s in shards])
     np.testing.assert_array_equal(kids, ref.population.candidates[64:])
+
+
+@pytest.mark.parametrize("cfg", ["c3"])
+def test_persistent_half_k_solve_matches_oracle(cfg):
+    """The reference's synthetic N-link arms have an all-zero left
+    half of Delta = Ad - I; the persistent solve then runs the half-K matvec.
+    Every final population cost must still match the FP64 oracle, and a
+    problem without that structure (random Ad) must take the full matvec."""
+    from paper_2001_04931_b200 import empc as E
+    from paper_2001_04931_b200 import workloads as W
+
+    w = W.WORKLOADS[cfg]
+    specs, x0s = W.build(w)
+    st = w.settings(generations=3)
+    res = P.solve_empc(specs[0], w.schedule(), st, x0s[0])
+    ctx = E._spec_context(specs[0], w.schedule(), st)
+    assert "halfK" in ctx.h.describe()
+    pr = O.Problem.from_spec(specs[0])
+    np.testing.assert_allclose(res.population.costs, O.rollout_costs(res.population.candidates, pr, x0s[0]),
+                               rtol=RTOL32)
+    # same shape, dense left half: the full matvec, and still the oracle's costs
+    rng = np.random.default_rng(3)
+    Ad = np.asarray(specs[0].model.Ad) + 1e-3 * rng.standard_normal(specs[0].model.Ad.shape)
+    spec2 = P.MpcSpec(P.DiscreteLinearModel(Ad, specs[0].model.Bd, specs[0].model.wd, specs[0].model.dt), w.T,
+                      Q=specs[0].Q, R=specs[0].R, x_goal=specs[0].x_goal, u_goal=specs[0].u_goal,
+                      u_min=specs[0].u_min, u_max=specs[0].u_max)
+    res2 = P.solve_empc(spec2, w.schedule(), st, x0s[0])
+    assert "halfK" not in E._spec_context(spec2, w.schedule(), st).h.describe()
+    pr2 = O.Problem.from_spec(spec2)
+    np.testing.assert_allclose(res2.population.costs, O.rollout_costs(res2.population.candidates, pr2, x0s[0]),
+                               rtol=RTOL32)
