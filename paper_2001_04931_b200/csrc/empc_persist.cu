@@ -19,7 +19,7 @@ template <>
 std::vector<PersistVariant<float>> persist_variants<float>() {
   return {PK(4, 1, 4, true, 1),  PK(8, 1, 4, true, 1),  PK(12, 2, 2, true, 1), PK(16, 2, 2, true, 1),
           PK(24, 2, 4, true, 2), PK(32, 2, 4, true, 2), PK(48, 2, 4, true, 2), PK(48, 1, 4, true, 1),
-          PKH(48, 2, 4, true, 2), PKH(32, 2, 4, true, 2)};
+          PKH(48, 2, 4, true, 2), PKH(48, 1, 4, true, 1), PKH(32, 2, 4, true, 2)};
 }
 
 template <>
