@@ -23,6 +23,7 @@ cpu_baseline / --impl reference = the reference algorithm (CPU oracle port
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import re
 import os
@@ -322,32 +323,46 @@ def run_ours(args):
         w_total.cand_steps_per_solve * args.steps)
     value = units_total / (total_ms * 1e-3)
 
-    # --- e2e through the public API (numpy in / numpy out)
+    # --- e2e through the public API (numpy in / numpy out).  Python objects
+    # alive at this point are frozen out of the cyclic GC (a full collection
+    # with torch loaded takes tens of ms); every call still allocates its
+    # own result arrays.  At least 100 calls for the sub-ms single problems.
+    n_e2e = args.steps if w.instances > 1 else max(args.steps, 100)
     e2e_times = []
     if w.instances > 1:
         batch.solve(x0s)
-        for _ in range(args.steps):
+        gc.collect()
+        gc.freeze()
+        for _ in range(n_e2e):
             t0 = time.perf_counter()
             r = batch.solve(x0s)
             e2e_times.append(time.perf_counter() - t0)
         h2d = batch.probs["Ad"].nbytes + sum(v.nbytes for k, v in batch.probs.items() if k != "Ad") + x0c.nbytes + sg.nbytes
         d2h = r.u.nbytes + r.best.nbytes + r.best_cost.nbytes + 4 * w.instances
     else:
-        for _ in range(3):
+        for _ in range(10):
             P.solve_empc(specs[0], sched, st, x0s[0])
-        for _ in range(args.steps):
+        gc.collect()
+        gc.freeze()
+        for _ in range(n_e2e):
             t0 = time.perf_counter()
             r = P.solve_empc(specs[0], sched, st, x0s[0])
             e2e_times.append(time.perf_counter() - t0)
         pa = E._problem_arrays(specs[0])
         h2d = sum(np.asarray(v).nbytes for v in pa.values()) + x0s[0].nbytes + sigma.nbytes + 32
         d2h = r.u.nbytes + r.best.nbytes + 8 + 4
+    gc.unfreeze()
     e2e_total = sum(e2e_times)
     if world > 1:
         t = torch.tensor([e2e_total], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = units_total / e2e_total
+    e2e_value = units_total * n_e2e / args.steps / e2e_total
+    e2e_ms = np.asarray(e2e_times) * 1e3
+    e2e_stats = {"calls": n_e2e, "latency_ms_median": float(np.median(e2e_ms)),
+                 "latency_ms_q1": float(np.percentile(e2e_ms, 25)), "latency_ms_q3": float(np.percentile(e2e_ms, 75)),
+                 "latency_ms_mean": float(e2e_ms.mean()), "latency_ms_max": float(e2e_ms.max()),
+                 "slowest_call": int(np.argmax(e2e_ms))}
 
     # --- roofline of the dominant kernel (rollout: K2+K3 with the K5 prologue)
     condensed = args.scorer == "condensed"
@@ -424,8 +439,7 @@ def run_ours(args):
                                 "recursion issues T n^2 of the 2 T n^2 algorithmic FLOP per candidate; achieved "
                                 "counts the algorithmic FLOP") if "halfK" in desc else None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "latency_ms_median": statistics.median(e2e_times) * 1e3, "api": "solve_empc" if w.instances == 1
-                else "EmpcBatch.solve"},
+                **e2e_stats, "api": "solve_empc" if w.instances == 1 else "EmpcBatch.solve"},
         "clocks": clocks,
         "gpu_launches": nlaunch * args.steps,
     }

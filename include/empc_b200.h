@@ -169,6 +169,21 @@ int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm);
  * (K/empc.py:85-119); see DESIGN.md §4.8. */
 int empc_set_tensor_cores(empc_handle* h, int32_t mode);
 
+/* Execution-path options (same results contract on every path; used by the
+ * parity tests to pin each path against the others):
+ *   EMPC_OPT_PERSISTENT  -1 auto (default: one cooperative launch per solve for
+ *                        single FP32 problems with n >= 24, i.e. C3), 0 per-
+ *                        generation launches, 1 persistent whenever the shape fits
+ *   EMPC_OPT_HALF_K      1 (default) skip the all-zero left half of the columns of
+ *                        Ad - I in the persistent recursion when present; 0 full matvec
+ *   EMPC_OPT_INCREMENTAL_SELECT 1 (default) after the first evolve rank only the
+ *                        elites + the children that beat the K-th elite; 0 rank all N
+ * empc_describe reports the path the last run took. */
+#define EMPC_OPT_PERSISTENT 1
+#define EMPC_OPT_HALF_K 2
+#define EMPC_OPT_INCREMENTAL_SELECT 3
+int empc_set_option(empc_handle* h, int32_t option, int32_t value);
+
 /* Population sharding over GPUs (K/empc.py:174-208 split
  * across ranks).  A rank holds the K elites (replicated) and the children of
  * global child indices [child_base, child_base + n_children) -- and, for the

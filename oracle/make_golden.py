@@ -204,12 +204,75 @@ def harness():
     print("wrote harness fixtures")
 
 
+def _digest(a) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def headline():
+    """Whole solves of the benchmark configs from the real reference
+    (K/empc.py:211-236) on the §8(d) systems: C3 (N=4096, K=256, G=10, cold +
+    warm), C4 at G=3 and two C5 instances.  Populations are large, so the
+    fixture keeps their SHA-256 (bit-identity checks), the costs, the elite
+    block of C3 and the best candidate; the draws are regenerated by the
+    oracle's RNG tap, which tests/test_oracle_golden.py pins to these files."""
+    condense, dynamics, empc, param = _import_ref()
+
+    def nlink_case(D, T, seed):
+        plant = dynamics.NLinkArm(dynamics.NLinkParams(links=D))
+        rng = np.random.default_rng(seed)
+        q0 = rng.uniform(-np.pi, np.pi, D)
+        qg = rng.uniform(-np.pi, np.pi, D)
+        x0 = np.concatenate([q0, np.zeros(D)])
+        xg = np.concatenate([qg, np.zeros(D)])
+        mdl = dynamics.discretize(dynamics.linearize(plant.ode, x0, np.zeros(D)), 0.01)
+        spec = condense.MpcSpec(mdl, T, Q=np.diag([10.0] * D + [0.1] * D), R=0.01 * np.eye(D),
+                                x_goal=xg, u_goal=np.zeros(D), u_min=np.full(D, -2.0), u_max=np.full(D, 2.0))
+        return spec, x0
+
+    cases = {
+        # name: (dof, T, p, N, K, G, system seeds, warm)
+        "c3_g10": (24, 50, 4, 4096, 256, 10, [0], True),
+        "c4_g3": (48, 200, 5, 16384, 1024, 3, [0], False),
+        "c5_i2": (12, 50, 3, 512, 32, 10, [0, 1], False),
+    }
+    for name, (D, T, p, N, K, G, seeds, warm) in cases.items():
+        st = empc.EmpcSettings(num_sims=N, num_parents=K, generations=G, seed=1)
+        sched = param.KnotSchedule(T=T, p=p)
+        d = dict(dof=np.int64(D), T=np.int64(T), p=np.int64(p), N=np.int64(N), K=np.int64(K), G=np.int64(G),
+                 seed=np.int64(1), seeds=np.array(seeds, np.int64))
+        for i, s in enumerate(seeds):
+            spec, x0 = nlink_case(D, T, s)
+            res = empc.solve_empc(spec, sched, st, x0)
+            pre = f"i{i}_"
+            d.update({pre + k: v for k, v in spec_arrays(spec).items()})
+            d.update({pre + "x0": x0, pre + "u": res.u, pre + "best": res.best,
+                      pre + "best_cost": np.float64(res.best_cost), pre + "pop_costs": res.population.costs,
+                      pre + "pop_sha": np.array(_digest(res.population.candidates)),
+                      pre + "pop_gen": np.int64(res.population.generation),
+                      pre + "sigma": empc._mutation_sigma(spec, st, x0)})
+            if name == "c3_g10":
+                d[pre + "pop_elites"] = res.population.candidates[:K]
+            if warm:
+                wr = empc.solve_empc(spec, sched, st, x0 + 0.01, prev=res.population)
+                d.update({pre + "warm_best": wr.best, pre + "warm_best_cost": np.float64(wr.best_cost),
+                          pre + "warm_pop_costs": wr.population.costs,
+                          pre + "warm_pop_sha": np.array(_digest(wr.population.candidates)),
+                          pre + "warm_gen": np.int64(wr.population.generation)})
+        np.savez_compressed(os.path.join(OUT, f"solve_{name}.npz"), **d)
+        print("wrote", name)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["closedloop"]:
         closed_loop()
     elif sys.argv[1:] == ["harness"]:
         harness()
+    elif sys.argv[1:] == ["headline"]:
+        headline()
     else:
         main()
         closed_loop()
         harness()
+        headline()

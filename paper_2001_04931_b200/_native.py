@@ -19,13 +19,14 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libempc_b20
 
 EMPC_OK, EMPC_EINVAL, EMPC_ECUDA, EMPC_ESTATE, EMPC_ENOMEM = 0, -1, -2, -3, -4
 EMPC_FP32, EMPC_FP64 = 0, 1
+EMPC_OPT_PERSISTENT, EMPC_OPT_HALF_K, EMPC_OPT_INCREMENTAL_SELECT = 1, 2, 3
 
 # every symbol include/empc_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "empc_create", "empc_destroy", "empc_last_error", "empc_set_schedule", "empc_set_scorer", "empc_set_problems",
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
-    "empc_set_variant", "empc_set_occupancy", "empc_set_tensor_cores", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
+    "empc_set_variant", "empc_set_occupancy", "empc_set_tensor_cores", "empc_set_option", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
     "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read",
     "empc_plant_linearize_discretize", "empc_plant_integrate", "empc_plant_last_error",
 )
@@ -113,6 +114,7 @@ def load(path: str | None = None):
         "empc_set_variant": (C.c_int, [P, I32]),
         "empc_set_occupancy": (C.c_int, [P, I32]),
         "empc_set_tensor_cores": (C.c_int, [P, I32]),
+        "empc_set_option": (C.c_int, [P, I32, I32]),
         "empc_philox": (C.c_int, [P, P, I32, P]),
         "empc_shard_setup": (C.c_int, [P, I64, I32, I64, I32, I32]),
         "empc_shard_entry_bytes": (C.c_int, [P, C.POINTER(I64)]),
@@ -203,6 +205,9 @@ class Handle:
 
     def set_tensor_cores(self, mode: int):
         self.call("empc_set_tensor_cores", int(mode))
+
+    def set_option(self, option: int, value: int):
+        self.call("empc_set_option", int(option), int(value))
 
 
 def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:

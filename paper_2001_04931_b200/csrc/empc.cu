@@ -85,6 +85,7 @@ class EngineBase {
   virtual void set_variant(int) = 0;
   virtual void set_occupancy(int) = 0;
   virtual void set_tensor_cores(int) = 0;
+  virtual void set_option(int, int) = 0;
   virtual void shard_setup(long long, int, long long, int, int) = 0;
   virtual size_t shard_entry_size() = 0;
   virtual void shard_init(const empc_run_args&) = 0;
@@ -111,7 +112,7 @@ class Engine final : public EngineBase {
     if (const char* v = std::getenv("EMPC_VARIANT")) forced_ = std::atoi(v);
     phases_ = std::getenv("EMPC_PHASES") != nullptr;
     incremental_ = std::getenv("EMPC_FULL_SELECT") == nullptr;
-    persist_enabled_ = std::getenv("EMPC_NO_PERSIST") == nullptr;
+    persist_mode_ = std::getenv("EMPC_NO_PERSIST") == nullptr ? -1 : 0;
     persist_ = persist_variants<S>();
     if (phases_) {
       dbg_n_ = (size_t)1 << 20;
@@ -344,8 +345,12 @@ class Engine final : public EngineBase {
         if (e / m != e % m && R[e] != 0.0) { rd = false; break; }
     }
     r_diag_ = rd;
-    // half-K: Delta = Ad - I has no nonzero entry in its left NP / 2 columns
-    bool hk = true;
+    // half-K: Delta = Ad - I has no nonzero entry in its left NP / 2 columns.
+    // Only the single-instance persistent solve uses it, so batched handles
+    // (C5: ~110 MB of staging) skip the scan.  The skipped block is exactly
+    // [0, NP/2): a state with n < NP (e.g. 13-15 DoF arms, NP = 32) has its
+    // zero position columns at [0, n/2) and keeps the full matvec.
+    bool hk = I_ == 1 && std::getenv("EMPC_NO_HALFK") == nullptr;
     for (int i = 0; i < I_ && hk; ++i) {
       const double* A = stage_prob_h_ + (size_t)i * SL_.stride + SL_.ad;
       for (int r = 0; r < n && hk; ++r)
@@ -631,12 +636,13 @@ class Engine final : public EngineBase {
   // tile co-resident): the whole run is one launch.  Returns false when the
   // configuration does not qualify and the per-generation launches are used.
   template <typename Pre, typename Post>
-  bool try_persistent(const empc_run_args& r, bool timed, Pre& pre, Post& post) {
+  bool try_persistent(const empc_run_args& r, bool timed, Pre& pre, Post& post,
+                      const std::vector<const void*>* inj = nullptr) {
     // small problems (n <= 16: C1, C2) run faster as per-generation launches
     // with several small CTAs per SM (profiles/bench_c1/c2): persistent only
-    // from NP = 24
-    if (!persist_enabled_ || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K ||
-        (d_.NP < 24 && forced_ < 0))
+    // from NP = 24 unless forced (EMPC_OPT_PERSISTENT = 1)
+    if (persist_mode_ == 0 || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K ||
+        (d_.NP < 24 && forced_ < 0 && persist_mode_ < 1))
       return false;
     const Variant<S>& v = pick();
     if (v.tc) return false;
@@ -675,7 +681,9 @@ class Engine final : public EngineBase {
     PersistArgs<S> P{};
     RolloutArgs<S>& a = P.ro;
     a.d = d_; a.SL = SL_; a.r_diag = r_diag_ ? 1 : 0;
-    a.mode = r.init ? kInitPhilox : kScore;
+    const S* inj_init = (inj && r.init) ? (const S*)(*inj)[0] : nullptr;
+    a.mode = r.init ? (inj_init ? kInitInject : kInitPhilox) : kScore;
+    a.inj_init = inj_init;
     a.nc = d_.N; a.row0 = 0; a.rows = d_.N;
     a.tile = tile0; a.tileP = tileP; a.tPS = tps_for(tileP); a.evolve = 0; a.cand_base = 0; a.copy_elites = 0;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
@@ -698,6 +706,12 @@ class Engine final : public EngineBase {
     P.qlist = qlist_;
     P.elite = elite_;
     P.out = out_d_;
+    if (inj && r.evolves > 0 && nc > 0) {  // the reference's draws (parity mode)
+      P.inj_parents = (const int*)(*inj)[1];
+      P.inj_take = (const uint8_t*)(*inj)[2];
+      P.inj_mut = (const uint8_t*)(*inj)[3];
+      P.inj_noise = (const double*)(*inj)[4];
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
@@ -734,7 +748,11 @@ class Engine final : public EngineBase {
     auto post = [&]() { if (timed_rollouts) CK(cudaEventRecord(ev_[2 * rollout_launches_ - 1], stream_)); };
     int cur = 0;
     const size_t pm = d_.pm;
-    if (inj == nullptr && try_persistent(r, timed_rollouts, pre, post)) return r.evolves & 1;
+    path_desc_ = "per-generation launches";
+    if (try_persistent(r, timed_rollouts, pre, post, inj)) {
+      path_desc_ = persist_desc_;
+      return r.evolves & 1;
+    }
     if (scorer_ == 1 && (r.init || r.rescore || r.evolves > 0)) launch_cond_build();
     if (r.init) {
       const S* inj_init = inj ? (const S*)(*inj)[0] : nullptr;
@@ -812,10 +830,10 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
   }
 
-  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int, bool>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int, bool, int, bool, bool>;
   GKey gkey(const empc_run_args& r, bool io) const {
     return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_,
-                           halfk_);
+                           halfk_, persist_mode_, halfk_ok_, incremental_);
   }
 
   // One graph per run shape.  io = true also captures the staging H2D copies
@@ -846,6 +864,7 @@ class Engine final : public EngineBase {
     graph_cur_[key] = cur;
     graph_launches_[key] = launches_;
     graph_rollouts_[key] = rollout_launches_;
+    graph_desc_[key] = path_desc_;
     return ge;
   }
 
@@ -889,6 +908,7 @@ class Engine final : public EngineBase {
     } else {
       cudaGraphExec_t ge = graph_for(r, true);
       cur = graph_cur_[gkey(r, true)];
+      path_desc_ = graph_desc_[gkey(r, true)];
       CK(cudaGraphLaunch(ge, stream_));
     }
     if (r.slot_out >= 0) {
@@ -962,6 +982,7 @@ class Engine final : public EngineBase {
     stage_run(r);
     cudaGraphExec_t ge = graph_for(r);
     const GKey key = gkey(r, false);
+    path_desc_ = graph_desc_[key];
     if (flush && !flush_) {
       flush_n_ = (size_t)256 << 20 >> 4;  // 256 MiB > 126 MB L2
       CK(cudaMalloc(&flush_, flush_n_ * 16));
@@ -1155,8 +1176,8 @@ class Engine final : public EngineBase {
     const Launch a = plan(v, d_.N - d_.K);
     char buf[512];
     std::snprintf(buf, sizeof buf, "%s | evolve tile=%d tileP=%d tiles=%d threads=%d smem=%zu | sms=%d%s%s", v.name,
-                  a.tile, a.tileP, a.tiles, a.threads, a.smem, sms_, persist_desc_.empty() ? "" : " | ",
-                  persist_desc_.c_str());
+                  a.tile, a.tileP, a.tiles, a.threads, a.smem, sms_, path_desc_.empty() ? "" : " | last run: ",
+                  path_desc_.c_str());
     return buf;
   }
   int num_variants() override { return (int)variants_.size(); }
@@ -1167,6 +1188,24 @@ class Engine final : public EngineBase {
   void set_tensor_cores(int mode) override {
     if (mode < -1 || mode > 1) throw InvalidArg{"tensor_cores must be -1 (auto), 0 (off) or 1 (on)"};
     tc_mode_ = mode;
+  }
+  void set_option(int opt, int val) override {
+    switch (opt) {
+      case EMPC_OPT_PERSISTENT:
+        if (val < -1 || val > 1) throw InvalidArg{"persistent mode must be -1 (auto), 0 (off) or 1 (on)"};
+        persist_mode_ = val;
+        break;
+      case EMPC_OPT_HALF_K:
+        if (val < 0 || val > 1) throw InvalidArg{"half-K must be 0 or 1"};
+        halfk_ok_ = val != 0;
+        break;
+      case EMPC_OPT_INCREMENTAL_SELECT:
+        if (val < 0 || val > 1) throw InvalidArg{"incremental selection must be 0 or 1"};
+        incremental_ = val != 0;
+        break;
+      default:
+        throw InvalidArg{"unknown option " + std::to_string(opt)};
+    }
   }
   void set_variant(int v) override {
     if (v >= (int)variants_.size()) throw InvalidArg{"variant out of range"};
@@ -1231,9 +1270,11 @@ class Engine final : public EngineBase {
   int sh_children_ = 0, sh_init_ = 0, sh_owns_elites_ = 0, sh_cur_ = 0;
   bool sh_init_phase_ = true, sh_on_ = false;
   bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
-  bool persist_enabled_ = true, persist_attr_set_ = false;
+  int persist_mode_ = -1;  // persistent solve: -1 auto, 0 off, 1 whenever the shape allows
+  bool persist_attr_set_ = false;
   std::vector<PersistVariant<S>> persist_;
-  std::string persist_desc_;
+  std::string persist_desc_, path_desc_;
+
   unsigned long long* dbg_ = nullptr;
   size_t dbg_n_ = 0;
   int dbg_ctas_ = 0;
@@ -1267,6 +1308,7 @@ class Engine final : public EngineBase {
   std::vector<cudaEvent_t> ev_;
   std::map<GKey, cudaGraphExec_t> graphs_;
   std::map<GKey, int> graph_cur_, graph_launches_, graph_rollouts_;
+  std::map<GKey, std::string> graph_desc_;
   int launches_ = 0, rollout_launches_ = 0;
 };
 
@@ -1405,6 +1447,7 @@ int empc_set_variant(empc_handle* h, int32_t variant) { GUARD(h, h->eng->set_var
 
 int empc_set_occupancy(empc_handle* h, int32_t ctas_per_sm) { GUARD(h, h->eng->set_occupancy(ctas_per_sm)); }
 int empc_set_tensor_cores(empc_handle* h, int32_t mode) { GUARD(h, h->eng->set_tensor_cores(mode)); }
+int empc_set_option(empc_handle* h, int32_t option, int32_t value) { GUARD(h, h->eng->set_option(option, value)); }
 
 int empc_shard_setup(empc_handle* h, int64_t child_base, int32_t n_children, int64_t init_base, int32_t n_init,
                      int32_t owns_elites) {

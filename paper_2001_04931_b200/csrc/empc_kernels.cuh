@@ -327,6 +327,8 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   constexpr int NPH = HK ? NP / KS / 2 : NP / KS;  // columns per reduction half
   constexpr int NJ = NPH / VEC;                    // 16-byte column groups per reduction half
   static_assert(!HK || (NP / 2) % (KS * VEC) == 0, "half-K split");
+  // NJ / jbase also drive the dense-Q matvecs (e'Qe needs every column)
+  static_assert(!(HK && DQ), "half-K is only valid with a diagonal Q");
   static_assert(!WS || 32 % (NRG * KS) == 0, "warp-synchronous variants need whole candidate groups per warp");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Dims& d = a.d;
@@ -1063,6 +1065,12 @@ struct PersistArgs {
   void* qlist;        // [2][qcap] (key, row) pairs
   int* elite;         // elite_idx (written by the selection)
   double* out;
+  // injected draws of the evolves (parity mode; NULL: in-kernel Philox):
+  // evolve g reads parents + g (N-K) 2, masks / noise + g (N-K) p m
+  const int* inj_parents;
+  const uint8_t* inj_take;
+  const uint8_t* inj_mut;
+  const double* inj_noise;
 };
 
 template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT, bool HK = false>
@@ -1085,7 +1093,14 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     EMPC_MARK(15)
     grid.sync();
     RolloutArgs<S> b = a;
-    b.mode = kBreedPhilox;
+    b.mode = P.inj_parents != nullptr ? kBreedInject : kBreedPhilox;
+    if (P.inj_parents != nullptr) {
+      const size_t per = (size_t)(N - K) * pm;
+      b.inj_parents = P.inj_parents + (size_t)g * (N - K) * 2;
+      b.inj_take = P.inj_take + (size_t)g * per;
+      b.inj_mut = P.inj_mut + (size_t)g * per;
+      b.inj_noise = P.inj_noise + (size_t)g * per;
+    }
     b.nc = N - K;
     b.row0 = K;
     b.tile = P.tile_evolve;

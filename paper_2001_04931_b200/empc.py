@@ -168,6 +168,12 @@ class _Context:
         self.h.call("empc_set_schedule", nat.iptr(np.ascontiguousarray(i1)), nat.iptr(np.ascontiguousarray(i2)),
                     nat.dptr(np.ascontiguousarray(c)))
         self.free = []
+        # two resident population slots (a result being read + the next
+        # solve's output): steady-state solves never allocate device memory
+        for _ in range(2):
+            v = nat.C.c_int32()
+            self.h.call("empc_pop_alloc", nat.C.byref(v))
+            self.free.append(v.value)
         self.args = nat.empc_run_args()
         self.scorer = 0
         self.tc = -1
@@ -481,9 +487,17 @@ class EmpcBatch:
             base = st.sigma_scale * (self.probs["u_max"] - self.probs["u_min"])
         err = self.probs["x_goal"] - x0s
         dist = np.linalg.norm(err, axis=1) / np.sqrt(self.n)
+        # rows whose scale factor is below one are recomputed with the exact
+        # per-instance expression of _mutation_sigma (the axis-wise norm can
+        # differ from it in the last bit); the rest are base * 1 either way
+        for i in np.flatnonzero(dist < st.dist_ref * (1.0 + 1e-9)):
+            dist[i] = float(np.linalg.norm(err[i])) / np.sqrt(err[i].size)
         return base * np.minimum(1.0, dist / st.dist_ref)[:, None]
 
-    def solve(self, x0s, prev: Population | None = None) -> BatchResult:
+    def solve(self, x0s, prev: Population | None = None, *, draws=None, init_candidates=None) -> BatchResult:
+        """``draws`` (one entry per evolve, each a list of per-instance draw
+        objects as in ``solve_empc``) and ``init_candidates`` (I, N, p, m)
+        inject the reference's random tensors (parity mode)."""
         x0s = nat.f64(np.asarray(x0s, float).reshape(self.I, self.n))
         st = self.settings
         if prev is None:
@@ -496,5 +510,27 @@ class EmpcBatch:
         self.ctx.set_problems(self.probs)
         self.ctx.set_scorer(self.scorer)
         self.ctx.set_tensor_cores(getattr(st, "tensor_cores", "auto"))
-        slot, u, best, bc, _ = _run(self.ctx, st, x0s, self.sigma(x0s), **kw)
+        inj, keep = None, []
+        if draws is not None or init_candidates is not None:
+            inj = nat.empc_injected()
+            if init_candidates is not None:
+                ic = nat.f64(init_candidates)
+                keep.append(ic)
+                inj.init = nat.dptr(ic)
+            if draws is not None and st.num_sims > st.num_parents and kw["evolves"] > 0:
+                stacked = [_StackedDraws(per) for per in draws]
+                i2, k2 = _draw_arrays(stacked, self.ctx)
+                inj.parents, inj.take_second, inj.mutate, inj.noise = i2.parents, i2.take_second, i2.mutate, i2.noise
+                keep.append(k2)
+        slot, u, best, bc, _ = _run(self.ctx, st, x0s, self.sigma(x0s), inject=inj, **kw)
+        del keep
         return BatchResult(u, best, bc, Population(generation=gen_end, _dev=(self.ctx, slot)))
+
+
+class _StackedDraws:
+    """Per-instance draw objects of one evolve stacked along a leading
+    instance axis (the C layout of ``empc_injected``)."""
+
+    def __init__(self, per_instance):
+        for f in ("parents", "take_second", "mutate", "noise"):
+            setattr(self, f, np.stack([np.asarray(getattr(d, f)) for d in per_instance]))

@@ -97,3 +97,25 @@ def test_qp_optimum_below_empc():
     pr, p = G.problem(g), int(g["p"])
     opt = O.qp_optimum(pr, p, g["x0"])
     assert opt <= float(g["best_cost"]) + 1e-9
+
+
+@pytest.mark.parametrize("name", ["c3_g10", "c4_g3", "c5_i2"])
+def test_headline_solves_match_reference(name):
+    """The benchmark configs (BASELINE configs C3, C4 at G=3, two C5
+    instances): the oracle's cold solve reproduces the real reference's
+    population bit for bit (SHA-256 of the FP64 candidates)."""
+    g = G.load("solve_" + name)
+    for i in range(len(g["seeds"])):
+        gi = G.instance(g, i)
+        pr, p, st = G.problem(gi), int(gi["p"]), G.settings(gi)
+        res = O.solve_empc(pr, p, st, gi["x0"])
+        assert G.digest(res.population.candidates) == str(gi["pop_sha"])
+        np.testing.assert_allclose(res.population.costs, gi["pop_costs"], rtol=1e-12)
+        np.testing.assert_array_equal(res.best, gi["best"])
+        np.testing.assert_array_equal(O.mutation_sigma(pr, st, gi["x0"]), gi["sigma"])
+        if "pop_elites" in gi:
+            np.testing.assert_array_equal(res.population.candidates[:st.num_parents], gi["pop_elites"])
+        if "warm_pop_sha" in gi:
+            warm = O.solve_empc(pr, p, st, gi["x0"] + 0.01, prev=res.population)
+            assert G.digest(warm.population.candidates) == str(gi["warm_pop_sha"])
+            np.testing.assert_array_equal(warm.best, gi["warm_best"])
