@@ -157,6 +157,9 @@ class Engine final : public EngineBase {
     CK(cudaMallocHost(&out_h_, sizeof(double) * (size_t)I_ * out_stride_));
     CK(cudaMalloc(&idx1_, sizeof(int) * d_.T));
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
+    CK(cudaMalloc(&seg_, sizeof(int) * d_.T));
+    if (const char* v = std::getenv("EMPC_STAGGER")) stagger_ = std::atoi(v);
+    if (const char* v = std::getenv("EMPC_WS_THREADS")) ws_threads_ = std::atoi(v);
     CK(cudaMalloc(&cw_, sizeof(S) * d_.T));
     CK(cudaMalloc(&G_, sizeof(S) * d_.p * d_.p));
     CK(cudaMalloc(&W64_, sizeof(double) * d_.T * d_.p));
@@ -180,7 +183,7 @@ class Engine final : public EngineBase {
     cudaFreeHost(stage_prob_h_); cudaFreeHost(stage_state_h_);
     for (int b = 0; b < 2; ++b) { cudaFree(pop_[b]); cudaFree(cost_[b]); }
     cudaFree(elite_); cudaFree(qcount_); cudaFree(qlist_); cudaFree(out_d_); cudaFreeHost(out_h_);
-    cudaFree(idx1_); cudaFree(idx2_); cudaFree(cw_); cudaFree(G_);
+    cudaFree(idx1_); cudaFree(idx2_); cudaFree(seg_); cudaFree(cw_); cudaFree(G_);
     cudaFree(W64_); cudaFree(G64_);
     if (cond_) cudaFree(cond_);
     if (cws_) cudaFree(cws_);
@@ -218,6 +221,11 @@ class Engine final : public EngineBase {
     CK(cudaMemcpy(G64_, G64.data(), sizeof(double) * p * p, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(idx1_, i1, sizeof(int) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(idx2_, i2, sizeof(int) * T, cudaMemcpyHostToDevice));
+    // runs of steps with the same knot pair: seg[k] = first step after k's run
+    std::vector<int> seg(T);
+    for (int k = T - 1; k >= 0; --k)
+      seg[k] = (k + 1 < T && i1[k + 1] == i1[k] && i2[k + 1] == i2[k]) ? seg[k + 1] : k + 1;
+    CK(cudaMemcpy(seg_, seg.data(), sizeof(int) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(cw_, cs.data(), sizeof(S) * T, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(G_, G.data(), sizeof(S) * p * p, cudaMemcpyHostToDevice));
     have_sched_ = true;
@@ -575,7 +583,8 @@ class Engine final : public EngineBase {
     a.tc_multi = L.multi;
     elites_copied_ = false;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
-    a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
+    a.idx1 = idx1_; a.idx2 = idx2_; a.seg = seg_; a.cw = cw_; a.G = G_;
+    a.stagger = stagger_;
     a.pop_in = pin; a.cost_in = cin; a.pop_out = pout; a.cost_out = cout;
     a.elite_idx = elite_; a.run = run_d_;
     a.inj_parents = inj_par; a.inj_take = inj_take; a.inj_mut = inj_mut; a.inj_noise = inj_noise; a.inj_init = inj_init;
@@ -649,12 +658,13 @@ class Engine final : public EngineBase {
     const PersistVariant<S>* pv = nullptr;
     const bool hk = halfk_ && halfk_ok_;
     for (auto& p : persist_)
-      if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws &&
+      if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && p.ws == v.ws &&
           p.hk == hk)
         pv = &p;
     if (!pv && hk)  // no half-K instantiation of this variant: the full matvec
       for (auto& p : persist_)
-        if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && !v.ws && !p.hk)
+        if (p.NP == v.NP && p.RR == v.RR && p.CC == v.CC && p.areg == v.areg && p.ks == v.ks && !v.dq && p.ws == v.ws &&
+            !p.hk)
           pv = &p;
     if (!pv) return false;
     const int nc = d_.N - d_.K;
@@ -665,8 +675,11 @@ class Engine final : public EngineBase {
     const int tileP = (std::max(tile0, Le.tile) + v.CC - 1) / v.CC * v.CC;
     const int NRG = v.NP / v.RR;
     const int nl = NRG * (tileP / v.CC);
-    const int threads = v.ks == 1 ? (nl + 31) / 32 * 32 : 2 * ((nl + 15) / 16 * 16);
-    if (threads > v.maxt) return false;
+    int threads = v.ks == 1 ? (nl + 31) / 32 * 32 : 2 * ((nl + 15) / 16 * 16);
+    // warp-synchronous CTAs carry helper warps for the breeding / staging
+    // phases (they skip the recursion)
+    if (v.ws) threads = std::max(threads, std::min(pv->maxt, ws_threads_) / 32 * 32);
+    if (threads > pv->maxt) return false;
     const size_t smem =
         smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq, select_smem_).total;
     if (smem > (size_t)kMaxSmem - 1024) return false;
@@ -687,7 +700,8 @@ class Engine final : public EngineBase {
     a.nc = d_.N; a.row0 = 0; a.rows = d_.N;
     a.tile = tile0; a.tileP = tileP; a.tPS = tps_for(tileP); a.evolve = 0; a.cand_base = 0; a.copy_elites = 0;
     a.prob = stage_prob_d_; a.state = stage_state_d_;
-    a.idx1 = idx1_; a.idx2 = idx2_; a.cw = cw_; a.G = G_;
+    a.idx1 = idx1_; a.idx2 = idx2_; a.seg = seg_; a.cw = cw_; a.G = G_;
+    a.stagger = stagger_;
     a.pop_in = pop_[0]; a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
     a.elite_idx = elite_; a.run = run_d_;
     a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
@@ -1288,7 +1302,9 @@ class Engine final : public EngineBase {
   int qcap_ = 0;
   double *out_d_ = nullptr, *out_h_ = nullptr;
   int out_stride_ = 0;
-  int *idx1_ = nullptr, *idx2_ = nullptr;
+  int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
+  int stagger_ = 0;       // WS recursion phase offset (cycles), EMPC_STAGGER
+  int ws_threads_ = 352;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)
   S *cw_ = nullptr, *G_ = nullptr;
   double *W64_ = nullptr, *G64_ = nullptr;  // FP64 W (T x p) and W'W for the condensed build
   int scorer_ = 0;

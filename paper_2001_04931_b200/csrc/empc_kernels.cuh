@@ -58,6 +58,7 @@ struct RolloutArgs {
   const double* state;  // FP64 state staging (x0, sigma), instances x SL.sstride
   const int* idx1;
   const int* idx2;
+  const int* seg;  // seg[k]: end (exclusive) of the run of steps with k's knot pair
   const S* cw;
   const S* G;  // W'W (p x p)
   const S* pop_in;
@@ -78,6 +79,7 @@ struct RolloutArgs {
   const double* cond;       // condensed scorer: per instance P, g, ref, J_ref (empc_cond.h)
   int cstride;              // doubles per instance of `cond`
   int tc_multi;             // tensor-core rollout: each CTA loops over tiles (Delta staged once per CTA)
+  int stagger;              // WS recursion: start delay (cycles) of warps 4-7 (sub-partition phase offset)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -119,7 +121,7 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.bs = persist_scratch ? al(bs * sizeof(S)) : 0;
   s.as = al((size_t)NP * NPS * sizeof(S));  // A staging (copied to registers by AREG variants)
   s.qs = dq ? al((size_t)NP * NPS * sizeof(S)) : 0;
-  s.sched = al((size_t)T * (2 * sizeof(int) + sizeof(S)));
+  s.sched = al((size_t)T * (3 * sizeof(int) + sizeof(S)));
   s.g = al((size_t)(p * p + 2) * sizeof(S));
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
@@ -352,7 +354,8 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   S* Qs = reinterpret_cast<S*>(ptr); ptr += sp.qs;    // [NP][NPS]
   int* sI1 = reinterpret_cast<int*>(ptr);
   int* sI2 = sI1 + T;
-  S* sC = reinterpret_cast<S*>(sI2 + T); ptr += sp.sched;
+  int* sSeg = sI2 + T;  // end of the knot segment starting at k
+  S* sC = reinterpret_cast<S*>(sSeg + T); ptr += sp.sched;
   S* sG = reinterpret_cast<S*>(ptr); ptr += sp.g;     // [p*p] + cost0
   ptr += sp.cu;  // per-candidate scratch slot of the plan (unused by this variant family)
   int* src = reinterpret_cast<int*>(ptr); ptr += sp.src;
@@ -377,6 +380,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     for (int k = tid; k < T; k += nthr) {
       sI1[k] = a.idx1[k];
       sI2[k] = a.idx2[k];
+      sSeg[k] = a.seg[k];
       sC[k] = a.cw[k];
     }
     for (int e = tid; e < p * p; e += nthr) sG[e] = a.G[e];
@@ -617,63 +621,88 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
 
   // ---- phase 3: horizon recursion in error coordinates,
   // e_{k+1} = e_k + Delta e_k + drive'_k (K/empc.py:110-112), state cost
-  // fused per step (K/empc.py:113-118).  The knot pair of the drive changes
-  // p - 1 times over the horizon: the endpoint b1 and slope b2 - b1 of the
-  // interpolation are cached in registers.
+  // fused per step (K/empc.py:113-118).  The knot pair (i1, i2) of the drive
+  // is constant over p - 1 segments of the horizon (sSeg[k] = end of the
+  // segment starting at k): the endpoint b1 and slope b2 - b1 of the
+  // interpolation are loaded once per segment, and the step loop carries no
+  // schedule test.  The state buffers ping-pong by swapping two offsets.
   // loop-invariant addresses: own / partner candidate rows of both buffers
   const S* xo0 = XC + (size_t)ce * NPS + jbase;
   const S* xp0 = XC + (size_t)(c0 + (ks ^ 1) * CH) * NPS + jbase;
-  const size_t bufstride = (size_t)tileP * NPS;
+  const int bufstride = tileP * NPS;
   S* xw0 = XC + (size_t)ce * NPS + rg;
-  int ci1 = -1, ci2 = -1;
-  S b1[RR][CH], db[RR][CH];
-  const int* __restrict__ si1 = sI1;
-  const int* __restrict__ si2 = sI2;
-  for (int k = 0; k < T; ++k) {
-    const size_t rd = (k & 1) ? bufstride : 0, wr = (k & 1) ? 0 : bufstride;
-    S ax[RR][CH];
-    EMPC_MATVEC(AREG, As, xo0 + rd, xp0 + rd, ax)
-    S qx[DQ ? RR : 1][DQ ? CH : 1];
-    if constexpr (DQ) EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qx)
-    const int i1 = si1[k], i2 = si2[k];
-    const S ck = sC[k];
-    if (i1 != ci1 || i2 != ci2) {  // uniform across the CTA
-      ci1 = i1;
-      ci2 = i2;
+  // diagonal Q: per-row sums of e_i^2, weighted by q_i once at the end
+  S srow[DQ ? 1 : RR][DQ ? 1 : CH];
 #pragma unroll
-      for (int r = 0; r < RR; ++r) {
-        S t2[CH];
-        lds_vec<S, CH>(BUT + (i1 * NP + rg + r * NRG) * tPS + ce, b1[r]);
-        lds_vec<S, CH>(BUT + (i2 * NP + rg + r * NRG) * tPS + ce, t2);
+  for (int r = 0; r < (DQ ? 1 : RR); ++r)
 #pragma unroll
-        for (int q = 0; q < CH; ++q) db[r][q] = t2[q] - b1[r][q];
+    for (int q = 0; q < (DQ ? 1 : CH); ++q) srow[r][q] = S(0);
+  // WS: whole warps without candidates (CTA helpers) skip the recursion, and
+  // warps 4-7 start `stagger` cycles late so that the two warps sharing an
+  // SM sub-partition run their latency-bound step tails out of phase
+  const bool run_loop = !WS || active;
+  if constexpr (WS) {
+    if (run_loop && a.stagger > 0 && ((warp >> 2) & 1)) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < a.stagger) {
       }
     }
-    S* xw = xw0 + wr;
+  }
+  int rdo = 0, wro = bufstride;
+  for (int k0 = 0; run_loop && k0 < T;) {
+    const int k1 = sSeg[k0];
+    const int i1 = sI1[k0], i2 = sI2[k0];
+    S b1[RR][CH], db[RR][CH];
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
+      S t2[CH];
+      lds_vec<S, CH>(BUT + (i1 * NP + rg + r * NRG) * tPS + ce, b1[r]);
+      lds_vec<S, CH>(BUT + (i2 * NP + rg + r * NRG) * tPS + ce, t2);
 #pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        if constexpr (DQ) cst[q] = fma(xo[r][q], qx[r][q], cst[q]);  // e_k' Q e_k
-        const S en = xo[r][q] + fma(ck, db[r][q], ax[r][q] + b1[r][q]);
-        xo[r][q] = en;
-        if constexpr (!DQ) cst[q] = fma(qv[r] * en, en, cst[q]);  // e_{k+1}' diag(Q) e_{k+1}
-#ifndef EMPC_EXP_NOSTS
-        if (active) xw[q * NPS + r * NRG] = en;
-#endif
-      }
+      for (int q = 0; q < CH; ++q) db[r][q] = t2[q] - b1[r][q];
     }
-    // WS: all rows of a candidate group live in one warp, so the state
-    // exchange of a step only needs a warp-level barrier and warps run
-    // their horizons independently
-#ifndef EMPC_EXP_NOBAR
-    if constexpr (WS) __syncwarp(); else __syncthreads();
+    for (int k = k0; k < k1; ++k) {
+      S ax[RR][CH];
+      EMPC_MATVEC(AREG, As, xo0 + rdo, xp0 + rdo, ax)
+      S qx[DQ ? RR : 1][DQ ? CH : 1];
+      if constexpr (DQ) EMPC_MATVEC(false, Qs, xo0 + rdo, xp0 + rdo, qx)
+      const S ck = sC[k];
+      S* xw = xw0 + wro;
+#pragma unroll
+      for (int r = 0; r < RR; ++r) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          if constexpr (DQ) cst[q] = fma(xo[r][q], qx[r][q], cst[q]);  // e_k' Q e_k
+          const S en = xo[r][q] + fma(ck, db[r][q], ax[r][q] + b1[r][q]);
+          xo[r][q] = en;
+          if constexpr (!DQ) srow[r][q] = fma(en, en, srow[r][q]);  // e_{k+1,i}^2
+#ifndef EMPC_EXP_NOSTS
+          if (active) xw[q * NPS + r * NRG] = en;
 #endif
+        }
+      }
+      const int t = rdo;
+      rdo = wro;
+      wro = t;
+      // WS: all rows of a candidate group live in one warp, so the state
+      // exchange of a step only needs a warp-level barrier and warps run
+      // their horizons independently
+#ifndef EMPC_EXP_NOBAR
+      if constexpr (WS) __syncwarp(); else __syncthreads();
+#endif
+    }
+    k0 = k1;
+  }
+  if constexpr (!DQ) {
+#pragma unroll
+    for (int r = 0; r < RR; ++r)
+#pragma unroll
+      for (int q = 0; q < CH; ++q) cst[q] = fma(qv[r], srow[r][q], cst[q]);  // diag(Q) e'e over k = 1..T
   }
   if constexpr (WS) __syncthreads();
   if constexpr (DQ) {
     // terminal state term e_T' Q e_T
-    const size_t rd = (T & 1) ? bufstride : 0;
+    const int rd = (T & 1) ? bufstride : 0;
     S qf[RR][CH];
     EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qf)
 #pragma unroll

@@ -51,6 +51,8 @@ struct PersistVariant {
   int ks;
   void (*kernel)(const PersistArgs<S>);
   bool hk = false;  // half-K matvec (left half of Delta's columns zero)
+  bool ws = false;  // warp-synchronous candidate groups (no CTA barrier per step)
+  int maxt = 1024;  // launch bound of the instantiation
 };
 
 template <typename S>
