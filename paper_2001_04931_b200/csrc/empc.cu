@@ -429,7 +429,8 @@ class Engine final : public EngineBase {
     return t;
   }
 
-  Launch plan(const Variant<S>& v, int nc, int cps_override = 0) const {
+  Launch plan(const Variant<S>& v, int nc, int cps_override = 0, int maxt_override = 0) const {
+    const int maxt = maxt_override > 0 ? maxt_override : v.maxt;
     if (v.tc) {  // tensor-core rollout: one MMA tile (128 candidates) per CTA
       Launch L{};
       // one instance: spread the candidates over all SMs (rows beyond the
@@ -458,7 +459,7 @@ class Engine final : public EngineBase {
     };
     auto fits = [&](int tileP) {
       const SmemPlan sp = smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq);
-      return sp.total <= (size_t)kMaxSmem && threads_for(tileP) <= v.maxt;
+      return sp.total <= (size_t)kMaxSmem && threads_for(tileP) <= maxt;
     };
     int maxP = CC;
     if (!fits(maxP)) throw InvalidArg{"problem too large for the rollout kernel (" + std::string(v.name) + ")"};
@@ -516,6 +517,11 @@ class Engine final : public EngineBase {
       } else if (d_.NP <= 16) {
         pref[0] = find(2, 2, true, 1);
         pref[1] = find(1, 4, true, 1);
+      } else if (d_.NP == 48 && I_ == 1) {
+        // warp-synchronous candidate groups + helper warps that draw the
+        // next generation during the recursion (persistent solve, C3)
+        pref[0] = find(3, 4, true, 2);
+        pref[1] = find(2, 4, true, 2);
       } else if (d_.NP <= 48 && I_ == 1) {
         pref[0] = find(2, 4, true, 2);
         pref[1] = find(1, 4, true, 1);
@@ -668,7 +674,7 @@ class Engine final : public EngineBase {
           pv = &p;
     if (!pv) return false;
     const int nc = d_.N - d_.K;
-    const Launch Le = plan(v, nc, 1);
+    const Launch Le = plan(v, nc, 1, pv->maxt);
     if (Le.tiles > sms_) return false;
     const int grid = Le.tiles;
     const int tile0 = (d_.N + grid - 1) / grid;
@@ -720,6 +726,10 @@ class Engine final : public EngineBase {
     P.qlist = qlist_;
     P.elite = elite_;
     P.out = out_d_;
+    {  // helper warps (WS variants) draw the next generation during the recursion
+      const int hstart = ((v.ks == 1 ? 1 : 2) * NRG * (tileP / v.CC) + 31) / 32 * 32;
+      P.predraw = (v.ws && threads > hstart && !inj && predraw_ok_) ? 1 : 0;
+    }
     if (inj && r.evolves > 0 && nc > 0) {  // the reference's draws (parity mode)
       P.inj_parents = (const int*)(*inj)[1];
       P.inj_take = (const uint8_t*)(*inj)[2];
@@ -742,7 +752,7 @@ class Engine final : public EngineBase {
     ++rollout_launches_;
     if (timed) post();
     persist_desc_ = std::string("persistent grid=") + std::to_string(grid) + " threads=" + std::to_string(threads) +
-                    " smem=" + std::to_string(smem) + (pv->hk ? " halfK" : "");
+                    " smem=" + std::to_string(smem) + (pv->hk ? " halfK" : "") + (P.predraw ? " predraw" : "");
     return true;
   }
 
@@ -826,8 +836,9 @@ class Engine final : public EngineBase {
     }
     run_h_->seed = r.seed;
     run_h_->gen0 = r.generation0;
-    run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 16));
-    run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 16));
+    // Bernoulli(p) as u32 < round(p 2^32): resolution 2^-32, p = 1 always
+    run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 32));
+    run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 32));
     if (copies) enqueue_h2d();
     if (!r.init) {
       Slot& s = slot(r.slot_in);
@@ -1304,6 +1315,7 @@ class Engine final : public EngineBase {
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
   int stagger_ = 0;       // WS recursion phase offset (cycles), EMPC_STAGGER
+  bool predraw_ok_ = std::getenv("EMPC_NO_PREDRAW") == nullptr;
   int ws_threads_ = 352;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)
   S *cw_ = nullptr, *G_ = nullptr;
   double *W64_ = nullptr, *G64_ = nullptr;  // FP64 W (T x p) and W'W for the condensed build

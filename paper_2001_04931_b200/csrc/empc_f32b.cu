@@ -14,7 +14,8 @@ static std::vector<Variant<float>> variants_f32_ffma(int NP) {
     case 48: return {FSMALL(48), RVK(float, 48, 2, 2, true, false, 2), RVK(float, 48, 2, 4, true, false, 2),
                      RVK(float, 48, 1, 4, true, false, 2), RVK(float, 48, 4, 4, false, false, 2),
                      RVK(float, 48, 4, 2, true, false, 2), RVK(float, 48, 4, 4, true, false, 2),
-                     RVW(float, 48, 3, 4, true, false, 2, true), RVW(float, 48, 3, 2, true, false, 2, true)};
+                     RVW(float, 48, 3, 4, true, false, 2, true), RVW(float, 48, 3, 2, true, false, 2, true),
+                     RVW(float, 48, 3, 1, true, false, 1, true), RVW(float, 48, 3, 2, true, false, 1, true)};
     case 64: return {RV(float, 64, 1, 4, true, false), RV(float, 64, 2, 2, true, false), RV(float, 64, 4, 4, false, false),
                      RV(float, 64, 4, 8, false, false), RV(float, 64, 4, 4, false, true)};
     case 96: return {RV(float, 96, 4, 4, false, false), RV(float, 96, 4, 8, false, false), RV(float, 96, 2, 4, false, false),

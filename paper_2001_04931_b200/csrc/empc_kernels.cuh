@@ -31,7 +31,7 @@ struct StageLayout {
 struct RunParams {
   uint64_t seed;
   int64_t gen0;
-  uint64_t thr_cross;  // crossover_prob * 2^16 (Bernoulli by a 16-bit uniform < thr)
+  uint64_t thr_cross;  // round(crossover_prob * 2^32): Bernoulli by a 32-bit uniform < thr
   uint64_t thr_mut;
 };
 
@@ -80,6 +80,12 @@ struct RolloutArgs {
   int cstride;              // doubles per instance of `cond`
   int tc_multi;             // tensor-core rollout: each CTA loops over tiles (Delta staged once per CTA)
   int stagger;              // WS recursion: start delay (cycles) of warps 4-7 (sub-partition phase offset)
+  // persistent solve:
+  int parents_from_out;     // elites already at rows [0, K) of pop_out (read parents there)
+  int draws_ready;          // phase 1a done for this tile (helper warps drew it in the previous generation)
+  int draw_next;            // helper warps draw evolve `draw_evolve`'s tile during the recursion
+  int draw_evolve;
+  int draw_tile0, draw_cnt; // that tile (children [draw_tile0, draw_tile0 + draw_cnt))
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -100,7 +106,7 @@ struct Geo {
 
 // Shared memory plan (host and device agree on it).
 struct SmemPlan {
-  size_t us, but, xc, as, qs, sched, g, cu, src, cv, bs, total;
+  size_t us, but, xc, as, qs, sched, g, cu, src, cv, bs, off, total;
 };
 
 template <typename S>
@@ -126,7 +132,10 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
   s.cu = al((size_t)tileP * sizeof(S));
   s.src = al((size_t)tileP * 2 * sizeof(int));
   s.cv = al((size_t)(4 * NP + 5 * m) * sizeof(S) + (size_t)tileP * p * m + 16);
-  s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv + s.bs;
+  // persistent solve: mutation offsets of the next generation's draws (the
+  // leading scratch is reused by the selection between generations)
+  s.off = persist_scratch ? al((size_t)p * m * tPS * sizeof(S)) : 0;
+  s.total = s.us + s.but + s.xc + s.as + s.qs + s.sched + s.g + s.cu + s.src + s.cv + s.bs + s.off;
   return s;
 }
 
@@ -139,20 +148,71 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
+// K5 random draws of one tile of children (K/empc.py:195-199), counter-based
+// Philox4x32-10 keyed by the 64-bit seed, by threads [t0, t0 + nt) of the CTA:
+//   parents: counter (0xFFFFFFFF, child, instance, generation), x / y ->
+//            two uniform elite ranks by Lemire's multiply-shift (K/empc.py:196);
+//   genes:   per PAIR of genes (2q, 2q+1) counter (q, child, instance,
+//            generation): x / y -> 32-bit crossover uniforms, z / w -> 32-bit
+//            mutation uniforms, Bernoulli by u32 < round(prob * 2^32)
+//            (K/empc.py:197-198); when either gene mutates, counter
+//            (q | 2^31, child, instance, generation): z / w -> a Box-Muller
+//            pair of standard normals scaled by sigma (K/empc.py:199, 202-203).
+// Writes src[2c..2c+1] (ranks), tbits[c * pm + g] and off[g * tPS + c].
+template <typename S>
+__device__ __forceinline__ void draw_tile(const RunParams& rp, uint32_t gen, int K, int pm, int m, int inst,
+                                          int cand0, int cnt, int tPS, int t0, int nt, int* src, uint8_t* tbits,
+                                          S* off, const S* csig) {
+  const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
+  for (int c = t0; c < cnt; c += nt) {
+    const U4 r = philox4x32_10(U4{kParentWord, (uint32_t)(cand0 + c), (uint32_t)inst, gen}, key0, key1);
+    src[2 * c] = (int)mulhi32(r.x, (uint32_t)K);
+    src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)K);
+  }
+  const int hp = (pm + 1) >> 1;
+  const uint64_t tc = rp.thr_cross, tm = rp.thr_mut;
+#pragma unroll 2
+  for (int e = t0; e < cnt * hp; e += nt) {
+    const int c = e / hp, q = e - c * hp;
+    const int g0 = 2 * q, g1 = g0 + 1;
+    const bool two = g1 < pm;
+    const int l0 = g0 % m;
+    const int l1 = (l0 + 1 == m) ? 0 : l0 + 1;
+    const uint32_t cand = (uint32_t)(cand0 + c);
+    const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, gen}, key0, key1);
+    const bool m0 = (uint64_t)r.z < tm, m1 = two && (uint64_t)r.w < tm;
+    S n0 = S(0), n1 = S(0);
+    if (m0 || m1) {
+      const U4 b = philox4x32_10(U4{(uint32_t)q | 0x80000000u, cand, (uint32_t)inst, gen}, key0, key1);
+      normal_pair<S>(b.z, b.w, n0, n1);
+    }
+    tbits[c * pm + g0] = (uint64_t)r.x < tc;
+    off[g0 * tPS + c] = m0 ? n0 * csig[l0] : S(0);
+    if (two) {
+      tbits[c * pm + g1] = (uint64_t)r.y < tc;
+      off[g1 * tPS + c] = m1 ? n1 * csig[l1] : S(0);
+    }
+  }
+}
+
 // K5 prologue shared by the rollout and the condensed scorer: random draws
-// (phase 1a, independent of the producer grid), then -- after the PDL wait --
-// the elite carry-over and the tile's candidate knots into UsT[gene][cand]
-// (phase 1b).  Returns false when the CTA has no candidates.
+// (phase 1a, independent of the producer grid; skipped when a.draws_ready --
+// the persistent solve's helper warps drew them during the previous
+// recursion), then -- after the PDL wait -- the elite carry-over and the
+// tile's candidate knots into UsT[gene][cand] (phase 1b).  `off` holds the
+// mutation offsets (UsT itself, or a dedicated buffer in the persistent
+// solve).  Returns false when the CTA has no candidates.
 template <typename S>
 __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, int tile0, int cnt, int tileP, int tPS,
                                            S* UsT, int* src, uint8_t* tbits, const S* cumin, const S* cumax,
-                                           const S* csig, size_t pop_base, bool elites = true) {
+                                           const S* csig, size_t pop_base, bool elites = true, S* off = nullptr) {
   const Dims& d = a.d;
   const int m = d.m, pm = d.pm;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const double* __restrict__ X = a.state + (size_t)inst * a.SL.sstride;
   const StageLayout& SL = a.SL;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
+  if (off == nullptr) off = UsT;
   // ---- phase 1a: random draws -- counter-based, so also independent of the
   // producer grid (the run parameters are staged by the host copy)
   const RunParams rp = *a.run;
@@ -160,58 +220,34 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
   const uint32_t gen = (uint32_t)(rp.gen0 + a.evolve);
   const bool philox_breed = a.mode == kBreedPhilox;
   if (cnt > 0) {
-    if (breed) {
-      // parents (K/empc.py:196): two uniform elite ranks per child
+    if (a.mode == kBreedInject) {
       for (int c = tid; c < cnt; c += nthr) {
-        const int child = tile0 + c;
-        const uint32_t gchild = (uint32_t)(a.cand_base + child);
-        if (a.mode == kBreedInject) {
-          const int* pp = a.inj_parents + ((size_t)inst * a.nc + child) * 2;
-          src[2 * c] = pp[0];
-          src[2 * c + 1] = pp[1];
-        } else {
-          const U4 r = philox4x32_10(U4{kParentWord, gchild, (uint32_t)inst, gen}, key0, key1);
-          src[2 * c] = (int)mulhi32(r.x, (uint32_t)d.K);  // Lemire multiply-shift
-          src[2 * c + 1] = (int)mulhi32(r.y, (uint32_t)d.K);
-        }
+        const int* pp = a.inj_parents + ((size_t)inst * a.nc + tile0 + c) * 2;
+        src[2 * c] = pp[0];
+        src[2 * c + 1] = pp[1];
       }
-    }
-    if (philox_breed || a.mode == kInitPhilox) {
-      // One Philox4x32-10 per PAIR of genes (2q, 2q+1) of a child (counter
-      // (q, child, instance, generation)): 16-bit crossover and mutation
-      // uniforms from words x and y (K/empc.py:197-198), a Box-Muller pair
-      // from z, w for the two mutation offsets (K/empc.py:199); or the two
-      // uniform initial knots from (x, y) and (z, w) (K/empc.py:170)
+    } else if (philox_breed) {
+      if (!a.draws_ready)
+        draw_tile<S>(rp, gen, d.K, pm, m, inst, a.cand_base + tile0, cnt, tPS, tid, nthr, src, tbits, off, csig);
+    } else if (a.mode == kInitPhilox) {
+      // two uniform initial knots per Philox call (K/empc.py:170): genes 2q
+      // from (x, y), 2q + 1 from (z, w), counter (q, cand, instance, "INIT")
       const int hp = (pm + 1) >> 1;
-      const uint32_t tc = (uint32_t)rp.thr_cross, tm = (uint32_t)rp.thr_mut;
 #pragma unroll 2
       for (int e = tid; e < cnt * hp; e += nthr) {
-        const int c = e / hp, q = e - (e / hp) * hp;
+        const int c = e / hp, q = e - c * hp;
         const int g0 = 2 * q, g1 = g0 + 1;
-        const bool two = g1 < pm;
         const int l0 = g0 % m;
         const int l1 = (l0 + 1 == m) ? 0 : l0 + 1;
         const uint32_t cand = (uint32_t)(a.cand_base + tile0 + c);
-        if (philox_breed) {
-          const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, gen}, key0, key1);
-          S n0, n1;
-          normal_pair<S>(r.z, r.w, n0, n1);
-          tbits[c * pm + g0] = (r.x & 0xFFFFu) < tc;
-          UsT[g0 * tPS + c] = (r.y & 0xFFFFu) < tm ? n0 * csig[l0] : S(0);
-          if (two) {
-            tbits[c * pm + g1] = (r.x >> 16) < tc;
-            UsT[g1 * tPS + c] = (r.y >> 16) < tm ? n1 * csig[l1] : S(0);
-          }
-        } else {
-          const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, kInitTag}, key0, key1);
-          const S lo0 = cumin[l0], hi0 = cumax[l0];
-          const S v0 = lo0 + (hi0 - lo0) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
-          UsT[g0 * tPS + c] = v0 > hi0 ? hi0 : v0;
-          if (two) {
-            const S lo1 = cumin[l1], hi1 = cumax[l1];
-            const S v1 = lo1 + (hi1 - lo1) * uniform01<S>(r.z, r.w);
-            UsT[g1 * tPS + c] = v1 > hi1 ? hi1 : v1;
-          }
+        const U4 r = philox4x32_10(U4{(uint32_t)q, cand, (uint32_t)inst, kInitTag}, key0, key1);
+        const S lo0 = cumin[l0], hi0 = cumax[l0];
+        const S v0 = lo0 + (hi0 - lo0) * uniform01<S>(r.x, r.y);  // numpy uniform(low, high)
+        UsT[g0 * tPS + c] = v0 > hi0 ? hi0 : v0;
+        if (g1 < pm) {
+          const S lo1 = cumin[l1], hi1 = cumax[l1];
+          const S v1 = lo1 + (hi1 - lo1) * uniform01<S>(r.z, r.w);
+          UsT[g1 * tPS + c] = v1 > hi1 ? hi1 : v1;
         }
       }
     }
@@ -234,7 +270,11 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
   }
   if (cnt <= 0) return false;
   EMPC_MARK(9)
-  if (breed) {
+  // parent rows: elite rank r is row elite_idx[r] of pop_in -- or row r of
+  // pop_out when the selection already carried the elites over (persistent
+  // solve: no dependent index load)
+  const S* __restrict__ parents = a.parents_from_out ? a.pop_out : a.pop_in;
+  if (breed && !a.parents_from_out) {
     for (int c = tid; c < cnt; c += nthr) {  // elite ranks -> population rows
       src[2 * c] = a.elite_idx[(size_t)inst * d.K + src[2 * c]];
       src[2 * c + 1] = a.elite_idx[(size_t)inst * d.K + src[2 * c + 1]];
@@ -251,9 +291,9 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
       const int c = e / pm, g = e - (e / pm) * pm;
       const int l = g % m;
       const bool take = tbits[e] != 0;
-      const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+      const S par = parents[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
       const S lo = cumin[l], hi = cumax[l];
-      S v = par + UsT[g * tPS + c];
+      S v = par + off[g * tPS + c];
       v = v < lo ? lo : (v > hi ? hi : v);
       a.pop_out[(pop_base + a.row0 + tile0 + c) * pm + g] = v;
       UsT[g * tPS + c] = v;
@@ -279,15 +319,15 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
       } else if (philox_breed) {
         // crossover, mutation, clip (K/empc.py:201-204)
         const bool take = tbits[e] != 0;
-        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+        const S par = parents[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
         const S lo = cumin[l], hi = cumax[l];
-        v = par + UsT[g * tPS + c];
+        v = par + off[g * tPS + c];
         v = v < lo ? lo : (v > hi ? hi : v);
       } else {
         // injected draws, with the reference's FP64 arithmetic child + mutate*noise*sigma
         const size_t gi = ((size_t)inst * a.nc + cand) * pm + g;
         const bool take = a.inj_take[gi] != 0, mut = a.inj_mut[gi] != 0;
-        const S par = a.pop_in[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
+        const S par = parents[(pop_base + src[2 * c + (take ? 1 : 0)]) * pm + g];
         const double nz = mut ? a.inj_noise[gi] * X[SL.sig + l] : 0.0;
         v = (S)((double)par + nz);
         const S lo = cumin[l], hi = cumax[l];
@@ -369,6 +409,8 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   S* csig = cumax + m;
   S* crd = csig + m;
   S* Bs = persist_scratch ? reinterpret_cast<S*>(ptr) : XC;  // [NP][m+1]
+  ptr += sp.bs;
+  S* Off = persist_scratch ? reinterpret_cast<S*>(ptr) : nullptr;  // [gene][tPS] mutation offsets
 
   const size_t pop_base = (size_t)inst * a.rows;
   const bool breed = (a.mode == kBreedPhilox || a.mode == kBreedInject);
@@ -443,7 +485,8 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   }
   EMPC_MARK(8)
   uint8_t* tbits = reinterpret_cast<uint8_t*>(cw_ + 4 * NP + 5 * m);  // crossover choice, 1 byte per gene
-  if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base)) return;
+  if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base, true, Off))
+    return;
   __syncthreads();
   EMPC_MARK(3)
 
@@ -640,12 +683,23 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   // WS: whole warps without candidates (CTA helpers) skip the recursion, and
   // warps 4-7 start `stagger` cycles late so that the two warps sharing an
   // SM sub-partition run their latency-bound step tails out of phase
-  const bool run_loop = !WS || active;
+  // (warp-uniform: a warp with any active group runs the loop; its inactive
+  // lanes shadow group 0 so that __syncwarp sees the full warp)
+  const bool run_loop = !WS || __any_sync(0xFFFFFFFFu, active);
   if constexpr (WS) {
     if (run_loop && a.stagger > 0 && ((warp >> 2) & 1)) {
       const long long t0 = clock64();
       while (clock64() - t0 < a.stagger) {
       }
+    }
+    // helper warps: the next evolve's K5 draws for this CTA's tile (counter
+    // based, so they do not depend on this generation), off the critical path
+    if (!run_loop && a.draw_next && a.draw_cnt > 0) {
+      constexpr int kLT = KS == 1 ? 1 : 2;
+      const int hstart = (kLT * NRG * (tileP / CC) + 31) / 32 * 32;
+      if (tid >= hstart)
+        draw_tile<S>(*a.run, (uint32_t)(a.run->gen0 + a.draw_evolve), d.K, d.pm, m, inst,
+                     a.cand_base + a.draw_tile0, a.draw_cnt, tPS, tid - hstart, nthr - hstart, src, tbits, Off, csig);
     }
   }
   int rdo = 0, wro = bufstride;
@@ -1094,6 +1148,7 @@ struct PersistArgs {
   void* qlist;        // [2][qcap] (key, row) pairs
   int* elite;         // elite_idx (written by the selection)
   double* out;
+  int predraw;        // WS variant with helper warps: next-generation draws during the recursion
   // injected draws of the evolves (parity mode; NULL: in-kernel Philox):
   // evolve g reads parents + g (N-K) 2, masks / noise + g (N-K) p m
   const int* inj_parents;
@@ -1109,6 +1164,12 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   const int N = a.d.N, K = a.d.K, pm = a.d.pm;
   using OT = typename std::conditional<sizeof(S) == 4, uint32_t, uint64_t>::type;
   const size_t qstride = (size_t)a.qcap * 2 * sizeof(OT);
+  const int nc = N - K;
+  const int dt0 = blockIdx.x * P.tile_evolve;
+  a.draw_next = P.predraw && P.evolves > 0;
+  a.draw_evolve = 0;
+  a.draw_tile0 = dt0;
+  a.draw_cnt = min(P.tile_evolve, nc - dt0);
   rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(a, true, P.scratch);
   int cur = 0;
   for (int g = 0; g < P.evolves; ++g) {
@@ -1135,6 +1196,12 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     b.tile = P.tile_evolve;
     b.evolve = g;
     b.copy_elites = 0;
+    b.parents_from_out = 1;
+    // the helpers of a CTA without init candidates never ran (it returned
+    // early), so its first evolve draws inline
+    b.draws_ready = P.predraw && (g > 0 || (int)blockIdx.x * a.tile < a.nc);
+    b.draw_next = P.predraw && g + 1 < P.evolves;
+    b.draw_evolve = g + 1;
     b.pop_in = P.pop[cur];
     b.cost_in = P.cost[cur];
     b.pop_out = P.pop[cur ^ 1];

@@ -27,7 +27,9 @@ std::vector<PersistVariant<float>> persist_variants<float>() {
   return {PK(4, 1, 4, true, 1),  PK(8, 1, 4, true, 1),  PK(12, 2, 2, true, 1), PK(16, 2, 2, true, 1),
           PK(24, 2, 4, true, 2), PK(32, 2, 4, true, 2), PK(48, 2, 4, true, 2), PK(48, 1, 4, true, 1),
           PKH(48, 2, 4, true, 2), PKH(48, 1, 4, true, 1), PKH(32, 2, 4, true, 2),
-          PKW(48, 3, 4, true, 2, false, 256), PKW(48, 3, 4, true, 2, true, 384)};
+          PKW(48, 3, 4, true, 2, false, 256), PKW(48, 3, 4, true, 2, true, 384),
+          // one warp = two candidate groups of 16 lanes x 3 rows, no split-K shuffle
+          PKW(48, 3, 1, true, 1, true, 448), PKW(48, 3, 2, true, 1, true, 384)};
 }
 
 template <>

@@ -467,6 +467,15 @@ def test_philox_breeding_matches_counter_model():
     _, _, mut, z = breed_draws(77, 3, N - K, pm, K, 0.5, 0.3)
     np.testing.assert_array_equal(kids != 0.0, mut)
     np.testing.assert_allclose(kids[mut], 0.25 * z[mut], rtol=2e-5, atol=1e-6)
+    # 32-bit Bernoulli thresholds: a mutation probability far below 2^-16
+    # still mutates at its rate (K/empc.py:198 compares 53-bit uniforms)
+    N2 = 20000
+    s = P.EmpcSettings(num_sims=N2, num_parents=K, seed=5, sigma_noise=np.full(4, 0.25), mutation_prob=2e-5)
+    pop = P.Population(np.zeros((N2, 5, 4)), np.arange(N2, dtype=float), 4)
+    kids = P.evolve_generation(pop, spec, sched, s, np.array([100.0, 0.0])).candidates[K:].reshape(N2 - K, pm)
+    _, _, mut, _ = breed_draws(5, 4, N2 - K, pm, K, 0.5, 2e-5)
+    np.testing.assert_array_equal(kids != 0.0, mut)
+    assert 0 < mut.sum() < 40
 
 
 def test_batched_instances_match_individual_solves():
