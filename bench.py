@@ -136,29 +136,89 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_solve_time(w, specs, x0s, budget_s, max_solves=None):
-    """Time the reference algorithm (oracle port of knotmpc.empc) on the host."""
+def cpu_reference_solve_time(w, specs, x0s, budget_s, max_solves=None, threads=None):
+    """Time the reference algorithm (oracle port of knotmpc.empc) on the host.
+    ``threads`` limits the OpenBLAS pool (threadpoolctl), None = all cores."""
     from oracle import empc_oracle as O
 
-    st = O.Settings(num_sims=w.N, num_parents=w.K, generations=w.G, seed=1)
-    pr = O.Problem.from_spec(specs[0])
-    x0 = x0s[0]
-    O.solve_empc(pr, w.p, st, x0)  # warm-up
-    times = []
-    t_start = time.perf_counter()
-    while not times or (time.perf_counter() - t_start < budget_s and (max_solves is None or len(times) < max_solves)):
-        i = len(times) % len(specs)
-        pr = O.Problem.from_spec(specs[i])
-        t0 = time.perf_counter()
-        O.solve_empc(pr, w.p, st, x0s[i])
-        times.append(time.perf_counter() - t0)
     try:
-        from threadpoolctl import threadpool_info
+        from threadpoolctl import threadpool_limits, threadpool_info
+    except ImportError:  # pragma: no cover
+        threadpool_limits = threadpool_info = None
+    import contextlib
 
-        threads = max([d.get("num_threads", 1) for d in threadpool_info() if d.get("internal_api") == "openblas"] or [1])
-    except Exception:
-        threads = os.cpu_count()
-    return times, threads
+    lim = threadpool_limits(limits=threads, user_api="blas") if (threads and threadpool_limits) else (
+        contextlib.nullcontext())
+    with lim:
+        st = O.Settings(num_sims=w.N, num_parents=w.K, generations=w.G, seed=1)
+        pr = O.Problem.from_spec(specs[0])
+        x0 = x0s[0]
+        O.solve_empc(pr, w.p, st, x0)  # warm-up
+        times = []
+        t_start = time.perf_counter()
+        while not times or (time.perf_counter() - t_start < budget_s and (max_solves is None or len(times) < max_solves)):
+            i = len(times) % len(specs)
+            pr = O.Problem.from_spec(specs[i])
+            t0 = time.perf_counter()
+            O.solve_empc(pr, w.p, st, x0s[i])
+            times.append(time.perf_counter() - t0)
+        used = threads
+        if used is None:
+            try:
+                used = max([d.get("num_threads", 1) for d in threadpool_info() if d.get("internal_api") == "openblas"]
+                           or [1])
+            except Exception:
+                used = os.cpu_count()
+    return times, used
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _pool_worker(task):
+    """One process of the C5 CPU baseline: solve instances [first, first+count)
+    of the workload with one BLAS thread (the K/bench.py:694-699 pattern)."""
+    name, first, count, budget = task
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    from oracle import empc_oracle as O
+    from paper_2001_04931_b200 import workloads as W
+
+    with threadpool_limits(limits=1, user_api="blas"):
+        w = W.WORKLOADS[name]
+        specs, x0s = W.build(w, first, count)
+        st = O.Settings(num_sims=w.N, num_parents=w.K, generations=w.G, seed=1)
+        done, t0 = 0, time.perf_counter()
+        while done < count and time.perf_counter() - t0 < budget:
+            O.solve_empc(O.Problem.from_spec(specs[done]), w.p, st, x0s[done])
+            done += 1
+        return done, time.perf_counter() - t0
+
+
+def cpu_pool_instances_per_s(name, budget_s):
+    """C5 reference baseline: one worker process per host core, each with one
+    BLAS thread, solving distinct instances for ``budget_s`` seconds
+    (K/bench.py:694-699).  Returns (instances/s over the pool, workers, solved)."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+
+    workers = os.cpu_count() or 1
+    per = 512  # instances handed to each worker (more than it finishes in the budget)
+    tasks = [(name, i * per, per, budget_s) for i in range(workers)]
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        res = list(ex.map(_pool_worker, tasks))
+    solved = sum(r[0] for r in res)
+    rate = sum(r[0] / r[1] for r in res if r[1] > 0)
+    return rate, workers, solved
 
 
 def run_reference(args):
@@ -167,27 +227,40 @@ def run_reference(args):
         return
     from paper_2001_04931_b200 import workloads as W
 
-    w, _, specs, x0s, _ = workload(args, 0, 1)
+    w = W.WORKLOADS[args.config]
+    if args.instances is not None:
+        w = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, instances=args.instances)
     per_instance = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, 1)
-    times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=1)
-    budget = 120.0 / max(w.instances, 1) if w.instances > 1 else 120.0
-    steps = max(1, min(args.steps, int(budget / max(times[0], 1e-6))))
+    specs, x0s = W.build(per_instance) if w.instances == 1 else W.build(W.WORKLOADS[args.config], 0, 1)
     warm = max(1, min(args.warmup, 3))
-    cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=warm)
-    times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=1e9, max_solves=steps)
-    # one step = one solve of the workload; for batched C5 the instances are
-    # solved one after another (the per-instance time scales linearly)
-    t_step = statistics.mean(times) * w.instances
-    value = per_instance.cand_steps_per_solve * w.instances / t_step
+    if w.instances > 1:
+        # independent instances: one worker per host core, one BLAS thread each
+        budget = max(5.0, min(60.0, 6.0 * args.steps))
+        rate, workers, solved = cpu_pool_instances_per_s(args.config, budget)
+        t_step = w.instances / rate
+        value = per_instance.cand_steps_per_solve * w.instances / t_step
+        times, threads = [t_step], workers
+        sample = (f"{solved} cold solves of distinct {args.config} instances by {workers} worker processes x 1 BLAS "
+                  f"thread in {budget:.0f}s (oracle port of knotmpc.empc; K/bench.py:694-699 pool pattern); "
+                  f"step = {w.instances} instances at the pool rate")
+    else:
+        times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=1)
+        budget = 120.0
+        steps = max(1, min(args.steps, int(budget / max(times[0], 1e-6))))
+        cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=0.0, max_solves=warm)
+        times, threads = cpu_reference_solve_time(per_instance, specs[:1], x0s[:1], budget_s=1e9, max_solves=steps)
+        t_step = statistics.mean(times)
+        value = per_instance.cand_steps_per_solve / t_step
+        sample = f"{len(times)} cold solves of one {args.config} instance (oracle port of knotmpc.empc: numpy Philox + condensed scoring)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(times),
-        "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong" if w.instances > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}", "dof": w.dof, "T": w.T, "p": w.p,
                    "N": w.N, "K": w.K, "G": w.G, "instances": w.instances},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} cold solves of one instance (oracle port of knotmpc.empc: numpy "
-                                   f"Philox + condensed scoring), scaled x{w.instances} instances"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model(), "cpu_count": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "latency_ms": {"median": statistics.median(times) * 1e3},
     }
@@ -216,16 +289,19 @@ def run_population_sharded(args, rank, world):
 
     for _ in range(max(args.warmup, 3)):
         solve_population_sharded(shard, x0s[0], all_gather)
+    # device time of each solve on the handle's stream (where the kernels and
+    # the NCCL exchange are enqueued), max over ranks below
+    stream = torch.cuda.ExternalStream(shard.stream_ptr)
     sampler = ClockSampler(0)
     times = []
     dist.barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(stream)
         u, best, cost = solve_population_sharded(shard, x0s[0], all_gather)
-        e1.record()
-        torch.cuda.synchronize()
+        e1.record(stream)
+        e1.synchronize()
         times.append(e0.elapsed_time(e1))
     dist.barrier()
     clocks = sampler.stop()
@@ -244,11 +320,39 @@ def run_population_sharded(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(sum(v.nbytes for v in x0s) + 8 * 9 * 96 * 96),
                 "d2h_bytes_per_step": int(u.nbytes + best.nbytes + 8), "api": "shard.solve_population_sharded"},
         "clocks": clocks,
-        "gpu_launches": (2 * w.G + 1) * args.steps,
+        "gpu_launches": 3 * w.G * args.steps,  # init + (G-1) x (export, import, evolve) + export + import
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def cpu_baseline(args, w, specs, x0s):
+    """The reference algorithm on this host's cores, next to the device run
+    (BASELINE.md §4): all BLAS threads and one BLAS thread for one instance;
+    C5 through a process pool of one worker per core."""
+    from paper_2001_04931_b200 import workloads as W
+
+    one = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, 1)
+    budget = args.cpu_sample_s
+    if w.instances > 1:
+        rate, workers, solved = cpu_pool_instances_per_s(args.config, budget)
+        value = one.cand_steps_per_solve * rate
+        return {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                "sample": f"{solved} cold solves of distinct {args.config} instances in {budget:.0f}s by {workers} "
+                          "worker processes x 1 BLAS thread (oracle port of knotmpc.empc, K/bench.py:694-699 pool)",
+                "instances_per_s": rate, "cpu_model": cpu_model(), "cpu_count": os.cpu_count()}
+    times, threads = cpu_reference_solve_time(one, specs[:1], x0s[:1], budget_s=0.65 * budget)
+    t1, _ = cpu_reference_solve_time(one, specs[:1], x0s[:1], budget_s=0.35 * budget, threads=1)
+    return {"value": one.cand_steps_per_solve / statistics.mean(times), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} cold solves of one {args.config} instance in {sum(times):.1f}s with all "
+                      f"OpenBLAS threads (oracle port of knotmpc.empc: numpy Philox RNG + condensed-quadratic "
+                      f"scoring); {len(t1)} more with one thread",
+            "ms_per_solve": statistics.mean(times) * 1e3, "ms_per_solve_median": statistics.median(times) * 1e3,
+            "single_thread": {"value": one.cand_steps_per_solve / statistics.mean(t1), "cores": 1,
+                              "ms_per_solve": statistics.mean(t1) * 1e3,
+                              "ms_per_solve_median": statistics.median(t1) * 1e3},
+            "cpu_model": cpu_model(), "cpu_count": os.cpu_count()}
 
 
 def run_ours(args):
@@ -444,26 +548,31 @@ def run_ours(args):
         "gpu_launches": nlaunch * args.steps,
     }
     if rank == 0 and not args.no_cpu_baseline:
-        from paper_2001_04931_b200 import workloads as W
-
-        one = W.Workload(w.name, w.dof, w.T, w.p, w.N, w.K, w.G, 1)
-        budget = args.cpu_sample_s
-        times, threads = cpu_reference_solve_time(one, specs[:1], x0s[:1], budget_s=budget)
-        cpu_val = one.cand_steps_per_solve / statistics.mean(times)
-        line["cpu_baseline"] = {
-            "value": cpu_val, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{len(times)} cold solves of one {args.config} instance in {sum(times):.1f}s (oracle port of "
-                      "knotmpc.empc: numpy Philox RNG + condensed-quadratic scoring, OpenBLAS threads)",
-            "ms_per_solve": statistics.mean(times) * 1e3,
-        }
+        line["cpu_baseline"] = cpu_baseline(args, w_total, specs, x0s)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """``bench.py --gpus N`` without a torchrun environment: start N ranks
+    (one process per GPU, 127.0.0.1 rendezvous) and relay rank 0's line."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

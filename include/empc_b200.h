@@ -196,6 +196,11 @@ int empc_set_option(empc_handle* h, int32_t option, int32_t value);
  * best); empc_shard_evolve breeds and scores this rank's children.  Keys use
  * global rows and the RNG counters global child indices, so the result is
  * identical to the unsharded solve for any world size. */
+/* The shard calls are ASYNCHRONOUS on the handle's stream (empc_get_stream):
+ * enqueue the collective on the same stream and a generation runs without a
+ * host synchronisation.  empc_shard_init stages the problem, x0, sigma and the
+ * RNG parameters once; empc_shard_evolve reads only args->generation0.
+ * empc_shard_import synchronises only when an output pointer is given. */
 int empc_shard_setup(empc_handle* h, int64_t child_base, int32_t n_children, int64_t init_base, int32_t n_init,
                      int32_t owns_elites);
 int empc_shard_entry_bytes(empc_handle* h, int64_t* bytes);
@@ -205,6 +210,9 @@ int empc_shard_import(empc_handle* h, const void* dev_all, int32_t world, double
                       double* best_cost, int64_t* best_row);
 int empc_shard_evolve(empc_handle* h, const empc_run_args* args);
 int empc_shard_read(empc_handle* h, double* cands, double* costs);
+/* The handle's CUDA stream (a cudaStream_t), for enqueueing collectives after
+ * empc_shard_export and before empc_shard_import. */
+int empc_get_stream(empc_handle* h, void** stream);
 
 /* Batched plant linearization + discretization on the device:
  * for each of `count` operating points (x[i], u[i]) of one plant, the

@@ -27,7 +27,7 @@ EXPORTS = (
     "empc_pop_alloc", "empc_pop_free", "empc_pop_read", "empc_pop_write", "empc_run", "empc_score",
     "empc_select", "empc_expand", "empc_time_device", "empc_describe", "empc_num_variants",
     "empc_set_variant", "empc_set_occupancy", "empc_set_tensor_cores", "empc_set_option", "empc_philox", "empc_shard_setup", "empc_shard_entry_bytes",
-    "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read",
+    "empc_shard_init", "empc_shard_export", "empc_shard_import", "empc_shard_evolve", "empc_shard_read", "empc_get_stream",
     "empc_plant_linearize_discretize", "empc_plant_integrate", "empc_plant_last_error",
 )
 
@@ -123,6 +123,7 @@ def load(path: str | None = None):
         "empc_shard_import": (C.c_int, [P, P, I32, D, D, D, C.POINTER(I64)]),
         "empc_shard_evolve": (C.c_int, [P, C.POINTER(empc_run_args)]),
         "empc_shard_read": (C.c_int, [P, D, D]),
+        "empc_get_stream": (C.c_int, [P, C.POINTER(P)]),
         "empc_plant_linearize_discretize": (C.c_int, [C.POINTER(empc_plant), I32, D, D, C.c_double, C.c_double,
                                                       I32, I32, D, D, D]),
         "empc_plant_integrate": (C.c_int, [C.POINTER(empc_plant), I32, D, D, C.c_double, I32, I32, D]),

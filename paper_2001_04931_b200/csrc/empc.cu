@@ -93,6 +93,7 @@ class EngineBase {
   virtual void shard_import(const void*, int, double*, double*, double*, long long*) = 0;
   virtual void shard_evolve(const empc_run_args&) = 0;
   virtual void shard_read(double*, double*) = 0;
+  virtual void* stream() = 0;
 };
 
 template <typename S>
@@ -1102,12 +1103,22 @@ class Engine final : public EngineBase {
   void shard_check() {
     if (!sh_on_) throw InvalidArg{"empc_shard_setup first"};
   }
+  // The per-generation shard calls only ENQUEUE work on the handle's stream
+  // (empc_get_stream): a rank's generation is export -> all-gather (NCCL on
+  // the same stream) -> import -> evolve with no host synchronisation.  The
+  // problem, x0, sigma and RNG parameters are staged once by shard_init.
   void shard_init(const empc_run_args& r) override {
     shard_check();
     empc_run_args rr = r;
     rr.init = 1;
     rr.slot_in = -1;
     stage_run(rr);
+    sh_gen0_ = r.generation0;
+    if (!sh_attr_set_) {
+      CK(cudaFuncSetAttribute(shard_export_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+      CK(cudaFuncSetAttribute(shard_import_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+      sh_attr_set_ = true;
+    }
     pdl_next_ = false;
     if (scorer_ == 1) launch_cond_build();
     cand_base_ = (int)sh_init_base_;
@@ -1116,7 +1127,7 @@ class Engine final : public EngineBase {
     pdl_next_ = false;
     sh_cur_ = 0;
     sh_init_phase_ = true;
-    CK(cudaStreamSynchronize(stream_));
+    CK(cudaGetLastError());
   }
   int rank_grid(int M) const { return std::max(1, std::min(sms_, (M + 15) / 16)); }
   void shard_export(void* dev_out) override {
@@ -1127,24 +1138,22 @@ class Engine final : public EngineBase {
     const int M = (incl ? d_.K : 0) + nl;
     const size_t smem = (size_t)M * (sizeof(typename OrdOf<S>::T) + 2 * sizeof(int));
     if (smem > (size_t)kMaxSmem - 1024) throw InvalidArg{"shard too large for the export kernel"};
-    CK(cudaFuncSetAttribute(shard_export_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
     shard_export_kernel<S><<<rank_grid(M), 256, smem, stream_>>>(pop_[sh_cur_], cost_[sh_cur_], d_.K, d_.pm, incl, nl,
                                                                   gbase, (unsigned char*)dev_out);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(stream_));
   }
   void shard_import(const void* dev_all, int world, double* u, double* best, double* cost, long long* grow) override {
     shard_check();
     const int M = world * d_.K;
     const size_t smem = (size_t)M * (sizeof(unsigned long long) + sizeof(unsigned));
     if (smem > (size_t)kMaxSmem - 1024) throw InvalidArg{"world * num_parents too large for the import kernel"};
-    CK(cudaFuncSetAttribute(shard_import_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
     shard_import_kernel<S><<<rank_grid(M), 256, smem, stream_>>>((const unsigned char*)dev_all, M, d_.K, d_.pm, d_.m,
                                                                   pop_[sh_cur_], cost_[sh_cur_], elite_, out_d_);
     CK(cudaGetLastError());
+    sh_init_phase_ = false;
+    if (!u && !best && !cost && !grow) return;  // mid-solve generation: nothing to read back
     CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * out_stride_, cudaMemcpyDeviceToHost, stream_));
     CK(cudaStreamSynchronize(stream_));
-    sh_init_phase_ = false;
     if (u) std::memcpy(u, out_h_, sizeof(double) * d_.m);
     if (best) std::memcpy(best, out_h_ + d_.m, sizeof(double) * d_.pm);
     if (cost) *cost = out_h_[d_.m + d_.pm];
@@ -1153,27 +1162,28 @@ class Engine final : public EngineBase {
   void shard_evolve(const empc_run_args& r) override {
     shard_check();
     if (sh_init_phase_) throw InvalidArg{"import the elites before evolving"};
-    empc_run_args rr = r;
-    rr.init = 1;  // staging only: the population stays where it is
-    stage_run(rr);
+    // RNG generation = staged gen0 + evolve index: no re-staging per generation
+    const long long ev = r.generation0 - sh_gen0_;
+    if (ev < 0 || ev > INT32_MAX) throw InvalidArg{"generation precedes the shard's init"};
     pdl_next_ = false;
-    if (scorer_ == 1) launch_cond_build();
     cand_base_ = (int)sh_child_base_;
     int* saved_q = qcount_;
     qcount_ = nullptr;
     const bool saved_inc = incremental_;
     incremental_ = false;
-    launch_rollout(kBreedPhilox, sh_children_, d_.K, d_.N, 0, pop_[sh_cur_], cost_[sh_cur_], pop_[sh_cur_ ^ 1],
+    launch_rollout(kBreedPhilox, sh_children_, d_.K, d_.N, (int)ev, pop_[sh_cur_], cost_[sh_cur_], pop_[sh_cur_ ^ 1],
                    cost_[sh_cur_ ^ 1]);
     incremental_ = saved_inc;
     qcount_ = saved_q;
     cand_base_ = 0;
     pdl_next_ = false;
     sh_cur_ ^= 1;
-    CK(cudaStreamSynchronize(stream_));
+    CK(cudaGetLastError());
   }
+  void* stream() override { return (void*)stream_; }
   void shard_read(double* cands, double* costs) override {
     shard_check();
+    CK(cudaStreamSynchronize(stream_));
     const size_t rows = (size_t)d_.K + (sh_init_phase_ ? sh_init_ : sh_children_);
     const size_t nc = rows * d_.pm;
     ensure_scratch_dbl(std::max(nc, rows));
@@ -1293,7 +1303,8 @@ class Engine final : public EngineBase {
   bool elites_copied_ = false;  // the last selection also carried the elites over
   long long sh_child_base_ = 0, sh_init_base_ = 0;
   int sh_children_ = 0, sh_init_ = 0, sh_owns_elites_ = 0, sh_cur_ = 0;
-  bool sh_init_phase_ = true, sh_on_ = false;
+  bool sh_init_phase_ = true, sh_on_ = false, sh_attr_set_ = false;
+  long long sh_gen0_ = 1;
   bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
   int persist_mode_ = -1;  // persistent solve: -1 auto, 0 off, 1 whenever the shape allows
   bool persist_attr_set_ = false;
@@ -1503,6 +1514,9 @@ int empc_shard_evolve(empc_handle* h, const empc_run_args* args) {
   GUARD(h, { if (!args) throw InvalidArg{"null args"}; h->eng->shard_evolve(*args); });
 }
 int empc_shard_read(empc_handle* h, double* cands, double* costs) { GUARD(h, h->eng->shard_read(cands, costs)); }
+int empc_get_stream(empc_handle* h, void** stream) {
+  GUARD(h, { if (!stream) throw InvalidArg{"null stream"}; *stream = h->eng->stream(); });
+}
 
 int empc_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out) {
   if (count <= 0) return EMPC_OK;

@@ -270,8 +270,9 @@ def _spec_context(spec, sched, settings, instances=1) -> _Context:
 
 def _device_population(ctx: _Context, pop: Population) -> _Slot:
     """Slot holding pop on ctx's device (uploads host-built populations)."""
-    if pop._dev is not None and pop._dev[0] is ctx:
-        return pop._dev[1]
+    dev = getattr(pop, "_dev", None)  # the reference's own Population has none
+    if dev is not None and dev[0] is ctx:
+        return dev[1]
     d = ctx.dims
     cands = nat.f64(pop.candidates).reshape(d.instances, d.num_sims, d.p, d.m)
     costs = nat.f64(pop.costs).reshape(d.instances, d.num_sims)

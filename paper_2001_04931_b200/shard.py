@@ -109,15 +109,35 @@ class PopulationShard:
         a.x0, a.sigma = nat.dptr(self._x0), nat.dptr(self._sg)
         return a
 
+    @property
+    def stream_ptr(self) -> int:
+        """The handle's CUDA stream: every shard call below only enqueues on it."""
+        v = self.C.c_void_p()
+        self.h.call("empc_get_stream", self.C.byref(v))
+        return v.value or 0
+
+    def sync(self):
+        import torch
+
+        torch.cuda.ExternalStream(self.stream_ptr).synchronize()
+
     def init(self, x0):
+        """Stage the problem, x0, sigma and the RNG parameters; score the
+        initial candidates (asynchronous)."""
         self.h.call("empc_shard_init", self.C.byref(self._run_args(x0, 1)))
 
     def export(self, device_ptr: int):
-        """Write this rank's top-K entries (K * entry_bytes) to device memory."""
+        """Enqueue this rank's top-K entries (K * entry_bytes) into device memory."""
         self.h.call("empc_shard_export", self.C.c_void_p(device_ptr))
 
-    def import_(self, device_ptr: int, world: int):
+    def import_(self, device_ptr: int, world: int, outputs: bool = True):
+        """Rank the W x K gathered entries and install the global top-K.  With
+        ``outputs`` (the last exchange of a solve) wait for it and return
+        (u, best, best_cost, global row); otherwise only enqueue."""
         nat, C = self.nat, self.C
+        if not outputs:
+            self.h.call("empc_shard_import", C.c_void_p(device_ptr), world, None, None, None, None)
+            return None
         u = np.empty(self.m)
         best = np.empty((self.p, self.m))
         cost = np.empty(1)
@@ -127,7 +147,11 @@ class PopulationShard:
         return u, best, float(cost[0]), row.value
 
     def evolve(self, x0, generation: int):
-        self.h.call("empc_shard_evolve", self.C.byref(self._run_args(x0, generation)))
+        """Breed and score this rank's children for ``generation`` (asynchronous;
+        x0 and sigma are the ones staged by init)."""
+        a = self._args
+        a.generation0 = int(generation)
+        self.h.call("empc_shard_evolve", self.C.byref(a))
 
     def local_population(self):
         """(candidates, costs) of rows [elites; this rank's children]."""
@@ -143,23 +167,26 @@ def solve_population_sharded(shard: PopulationShard, x0, all_gather):
     init + (G-1) x [exchange, select, breed] + a final exchange for the best.
 
     ``all_gather(local_uint8_tensor) -> gathered_uint8_tensor`` concatenates
-    every rank's export in rank order (e.g. ``dist.all_gather_into_tensor`` over
-    NCCL).  Returns (u, best, best_cost)."""
+    every rank's export in rank order.  It runs with the handle's stream as
+    torch's current stream, so ``dist.all_gather_into_tensor`` over NCCL is
+    stream-ordered between the export and the import: a generation is enqueued
+    back to back with no host synchronisation (a gloo exchange through host
+    copies also works, synchronously).  Returns (u, best, best_cost)."""
     import torch
 
     K, eb = shard.K, shard.entry_bytes
-    local = torch.empty(K * eb, dtype=torch.uint8, device="cuda")
-    shard.init(x0)
-    for g in range(1, shard.settings.generations):
+    stream = torch.cuda.ExternalStream(shard.stream_ptr)
+    with torch.cuda.stream(stream):
+        local = torch.empty(K * eb, dtype=torch.uint8, device="cuda")
+        shard.init(x0)
+        for g in range(1, shard.settings.generations):
+            shard.export(local.data_ptr())
+            gathered = all_gather(local)
+            shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb), outputs=False)
+            shard.evolve(x0, g)
         shard.export(local.data_ptr())
         gathered = all_gather(local)
-        torch.cuda.synchronize()
-        shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb))
-        shard.evolve(x0, g)
-    shard.export(local.data_ptr())
-    gathered = all_gather(local)
-    torch.cuda.synchronize()
-    u, best, cost, _ = shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb))
+        u, best, cost, _ = shard.import_(gathered.data_ptr(), gathered.numel() // (K * eb))
     return u, best, cost
 
 
@@ -175,6 +202,7 @@ def solve_population_emulated(spec, sched, settings, x0, world: int):
     def exchange():
         for s, b in zip(shards, bufs):
             s.export(b.data_ptr())
+            s.sync()
         allb = torch.cat(bufs)
         torch.cuda.synchronize()
         return [s.import_(allb.data_ptr(), world) for s in shards]
