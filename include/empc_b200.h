@@ -178,10 +178,21 @@ int empc_set_tensor_cores(empc_handle* h, int32_t mode);
  *                        Ad - I in the persistent recursion when present; 0 full matvec
  *   EMPC_OPT_INCREMENTAL_SELECT 1 (default) after the first evolve rank only the
  *                        elites + the children that beat the K-th elite; 0 rank all N
+ *   EMPC_OPT_RADIX_SELECT 1: per-generation selection by radix select of the K-th
+ *                        key and ranking of the K elites (default for single FP32
+ *                        populations with N >= 8192, e.g. C4); 0: rank by counting
+ *   EMPC_OPT_SMALL_SOLVE -1 auto (default: n <= 8 with little work, e.g. C1), 0 off,
+ *                        1 whenever it fits: the whole solve in ONE CTA per instance
+ *                        with the population resident in shared memory
+ *   EMPC_OPT_PERSIST_TILE minimum candidates per CTA of the persistent solve (0
+ *                        = one wave over the SMs; larger = fewer CTAs, cheaper grid syncs)
  * empc_describe reports the path the last run took. */
 #define EMPC_OPT_PERSISTENT 1
 #define EMPC_OPT_HALF_K 2
 #define EMPC_OPT_INCREMENTAL_SELECT 3
+#define EMPC_OPT_RADIX_SELECT 4
+#define EMPC_OPT_PERSIST_TILE 5
+#define EMPC_OPT_SMALL_SOLVE 6
 int empc_set_option(empc_handle* h, int32_t option, int32_t value);
 
 /* Population sharding over GPUs (K/empc.py:174-208 split

@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libempc_b20
 
 EMPC_OK, EMPC_EINVAL, EMPC_ECUDA, EMPC_ESTATE, EMPC_ENOMEM = 0, -1, -2, -3, -4
 EMPC_FP32, EMPC_FP64 = 0, 1
-EMPC_OPT_PERSISTENT, EMPC_OPT_HALF_K, EMPC_OPT_INCREMENTAL_SELECT = 1, 2, 3
+EMPC_OPT_PERSISTENT, EMPC_OPT_HALF_K, EMPC_OPT_INCREMENTAL_SELECT, EMPC_OPT_RADIX_SELECT = 1, 2, 3, 4
+EMPC_OPT_PERSIST_TILE, EMPC_OPT_SMALL_SOLVE = 5, 6
 
 # every symbol include/empc_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -25,6 +25,7 @@
 #include "empc_cond.h"
 #include "empc_variants.h"
 #include "empc_tc_rollout.cuh"
+#include "empc_small.h"
 
 using namespace empc;
 
@@ -161,6 +162,10 @@ class Engine final : public EngineBase {
     CK(cudaMalloc(&seg_, sizeof(int) * d_.T));
     if (const char* v = std::getenv("EMPC_STAGGER")) stagger_ = std::atoi(v);
     if (const char* v = std::getenv("EMPC_WS_THREADS")) ws_threads_ = std::atoi(v);
+    if (const char* v = std::getenv("EMPC_PERSIST")) persist_mode_ = std::atoi(v);
+    if (const char* v = std::getenv("EMPC_PERSIST_TILE")) persist_tile_ = std::atoi(v);
+    if (const char* v = std::getenv("EMPC_SMALL")) small_mode_ = std::atoi(v);
+    if (const char* v = std::getenv("EMPC_SMALL_THREADS")) small_threads_ = std::atoi(v);
     CK(cudaMalloc(&cw_, sizeof(S) * d_.T));
     CK(cudaMalloc(&G_, sizeof(S) * d_.p * d_.p));
     CK(cudaMalloc(&W64_, sizeof(double) * d_.T * d_.p));
@@ -170,6 +175,15 @@ class Engine final : public EngineBase {
     if (select_smem_ > (size_t)kMaxSmem - 1024) throw InvalidArg{"num_sims too large for the selection kernel"};
     // function attributes are process-wide: always the maximum, never a per-engine size
     CK(cudaFuncSetAttribute(select_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+    // large single populations (C4): radix select of the K-th key + ranking
+    // of the K elites only (O(M) + O(K^2) instead of O(M^2) per selection)
+    {
+      const char* e = std::getenv("EMPC_RADIX_SELECT");
+      const int min_n = e ? std::atoi(e) : 8192;
+      use_radix_ = sizeof(S) == 4 && I_ == 1 && min_n > 0 && d_.N >= min_n &&
+                   radix_select_smem(d_.N, d_.K) <= (size_t)kMaxSmem - 1024;
+      CK(cudaFuncSetAttribute(select_radix_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+    }
     for (auto& v : variants_) CK(cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CK(cudaFuncSetAttribute(ck_.score_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CK(cudaFuncSetAttribute(ck_.score_glob, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -430,7 +444,7 @@ class Engine final : public EngineBase {
     return t;
   }
 
-  Launch plan(const Variant<S>& v, int nc, int cps_override = 0, int maxt_override = 0) const {
+  Launch plan(const Variant<S>& v, int nc, int cps_override = 0, int maxt_override = 0, int min_tile = 0) const {
     const int maxt = maxt_override > 0 ? maxt_override : v.maxt;
     if (v.tc) {  // tensor-core rollout: one MMA tile (128 candidates) per CTA
       Launch L{};
@@ -473,6 +487,7 @@ class Engine final : public EngineBase {
       // warps each step, so the SM interleaves independent step pipelines
       const int cps = std::max(1, cps_override > 0 ? cps_override : (cps_ > 0 ? cps_ : default_cps(v, nc)));
       int tile = (nc + sms_ * cps - 1) / (sms_ * cps);
+      tile = std::max(tile, min_tile);     // fewer, larger CTAs (small persistent solves)
       if (tile > maxP) tile = maxP;        // several waves when smem / threads limit the tile
       int tiles = (nc + tile - 1) / tile;
       tile = (nc + tiles - 1) / tiles;     // balance
@@ -502,9 +517,10 @@ class Engine final : public EngineBase {
   // n <= 48, A in registers for batched small problems, smem A for n >= 64.
   const Variant<S>& pick() {
     if (forced_ >= 0) return variants_.at(forced_);
-    auto find = [&](int RR, int CC, bool areg, int ks) -> const Variant<S>* {
+    auto find = [&](int RR, int CC, bool areg, int ks, bool ws = false) -> const Variant<S>* {
       for (auto& v : variants_)
-        if (!v.tc && v.RR == RR && v.CC == CC && v.areg == areg && v.ks == ks && v.dq == dense_) return &v;
+        if (!v.tc && v.RR == RR && v.CC == CC && v.areg == areg && v.ks == ks && v.ws == ws && v.dq == dense_)
+          return &v;
       return nullptr;
     };
     if (use_tc()) {
@@ -521,7 +537,7 @@ class Engine final : public EngineBase {
       } else if (d_.NP == 48 && I_ == 1) {
         // warp-synchronous candidate groups + helper warps that draw the
         // next generation during the recursion (persistent solve, C3)
-        pref[0] = find(3, 4, true, 2);
+        pref[0] = find(3, 4, true, 2, true);
         pref[1] = find(2, 4, true, 2);
       } else if (d_.NP <= 48 && I_ == 1) {
         pref[0] = find(2, 4, true, 2);
@@ -642,8 +658,12 @@ class Engine final : public EngineBase {
     int* qin = incremental ? qcount_ + (size_t)((g - 1) & 1) * I_ : nullptr;
     const void* lin = (const char*)qlist_ + (size_t)((g - 1) & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
     int* qnext = qcount_ + (size_t)(g & 1) * I_;
-    launch_ex(select_kernel<S>, dim3(ctas, I_), dim3(256), select_smem_, pdl_next_, costs, N, d_.K, elite_, incremental,
-              qin, lin, qnext, qcap_, pop_in, pop_out, cost_out, d_.pm);
+    if (use_radix_)
+      launch_ex(select_radix_kernel<S>, dim3(ctas, I_), dim3(1024), radix_select_smem(N, d_.K), pdl_next_, costs, N,
+                d_.K, elite_, incremental, qin, lin, qnext, qcap_, pop_in, pop_out, cost_out, d_.pm);
+    else
+      launch_ex(select_kernel<S>, dim3(ctas, I_), dim3(256), select_smem_, pdl_next_, costs, N, d_.K, elite_,
+                incremental, qin, lin, qnext, qcap_, pop_in, pop_out, cost_out, d_.pm);
     pdl_next_ = use_pdl_;
     ++launches_;
   }
@@ -675,7 +695,7 @@ class Engine final : public EngineBase {
           pv = &p;
     if (!pv) return false;
     const int nc = d_.N - d_.K;
-    const Launch Le = plan(v, nc, 1, pv->maxt);
+    const Launch Le = plan(v, nc, 1, pv->maxt, persist_tile_);
     if (Le.tiles > sms_) return false;
     const int grid = Le.tiles;
     const int tile0 = (d_.N + grid - 1) / grid;
@@ -757,6 +777,51 @@ class Engine final : public EngineBase {
     return true;
   }
 
+  // Small problems (C1): the whole solve in one CTA per instance with the
+  // population resident in shared memory (empc_small.cu).  Auto: n <= 8, a
+  // diagonal Q, the rollout scorer and little work per generation.
+  template <typename Pre, typename Post>
+  bool try_small(const empc_run_args& r, bool timed, Pre& pre, Post& post, const std::vector<const void*>* inj) {
+    if (small_mode_ == 0 || scorer_ != 0 || dense_ || cps_ > 0 || (forced_ >= 0 && small_mode_ < 1)) return false;
+    const SmallKernel<S> kern = small_kernel<S>(d_.n);
+    if (kern == nullptr || d_.N > 4096) return false;
+    const size_t smem = small_smem<S>(d_.n, d_.m, d_.T, d_.p, d_.N, d_.K);
+    if (smem > (size_t)kMaxSmem) return false;
+    const int npv = d_.n <= 4 ? 4 : 8;
+    const long long work = (long long)d_.N * d_.T * npv * npv;
+    if (small_mode_ < 0 && work > (1LL << 18)) return false;
+    if (!small_attr_set_) {
+      CK(cudaFuncSetAttribute(small_kernel<S>(4), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+      CK(cudaFuncSetAttribute(small_kernel<S>(8), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+      small_attr_set_ = true;
+    }
+    SmallArgs<S> A{};
+    A.d = d_; A.SL = SL_; A.evolves = r.evolves; A.r_diag = r_diag_ ? 1 : 0;
+    A.prob = stage_prob_d_; A.state = stage_state_d_; A.run = run_d_;
+    A.idx1 = idx1_; A.idx2 = idx2_; A.seg = seg_; A.cw = cw_; A.G = G_;
+    A.pop_io = pop_[0]; A.cost_io = cost_[0]; A.out = out_d_;
+    A.mode = r.init ? kInitPhilox : (r.rescore ? kScore : kSmallResident);
+    if (inj && r.init) {
+      A.inj_init = (const S*)(*inj)[0];
+      A.mode = kInitInject;
+    }
+    if (inj && r.evolves > 0 && d_.N > d_.K) {
+      A.inj_parents = (const int*)(*inj)[1];
+      A.inj_take = (const uint8_t*)(*inj)[2];
+      A.inj_mut = (const uint8_t*)(*inj)[3];
+      A.inj_noise = (const double*)(*inj)[4];
+    }
+    // (draws and selection use every thread; scoring one thread per candidate)
+    const int threads = std::min(512, std::max(small_threads_, (d_.N + 31) / 32 * 32));
+    if (timed) pre();
+    launch_ex(kern, dim3(I_), dim3(threads), smem, false, A);
+    ++launches_;
+    ++rollout_launches_;
+    if (timed) post();
+    small_desc_ = "resident single-CTA solve threads=" + std::to_string(threads) + " smem=" + std::to_string(smem);
+    return true;
+  }
+
   // The device part of a run: prep, optional init / rescore, evolves, finalize.
   // Returns the index (0/1) of the buffer holding the final population.
   int enqueue_core(const empc_run_args& r, const std::vector<const void*>* inj, bool timed_rollouts = false) {
@@ -774,6 +839,10 @@ class Engine final : public EngineBase {
     int cur = 0;
     const size_t pm = d_.pm;
     path_desc_ = "per-generation launches";
+    if (try_small(r, timed_rollouts, pre, post, inj)) {
+      path_desc_ = small_desc_;
+      return 0;
+    }
     if (try_persistent(r, timed_rollouts, pre, post, inj)) {
       path_desc_ = persist_desc_;
       return r.evolves & 1;
@@ -856,10 +925,11 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
   }
 
-  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int, bool, int, bool, bool>;
+  using GKey = std::tuple<bool, bool, int, int, bool, int, int, bool, int, bool, int, bool, int>;
   GKey gkey(const empc_run_args& r, bool io) const {
     return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_,
-                           halfk_, persist_mode_, halfk_ok_, incremental_);
+                           halfk_, persist_mode_ + 4 * persist_tile_ + (small_mode_ + 1) * (1 << 24), halfk_ok_,
+                           (incremental_ ? 1 : 0) | (use_radix_ ? 2 : 0));
   }
 
   // One graph per run shape.  io = true also captures the staging H2D copies
@@ -1238,6 +1308,20 @@ class Engine final : public EngineBase {
         if (val < 0 || val > 1) throw InvalidArg{"incremental selection must be 0 or 1"};
         incremental_ = val != 0;
         break;
+      case EMPC_OPT_PERSIST_TILE:
+        if (val < 0 || val > 1 << 20) throw InvalidArg{"persistent tile out of range"};
+        persist_tile_ = val;
+        break;
+      case EMPC_OPT_SMALL_SOLVE:
+        if (val < -1 || val > 1) throw InvalidArg{"small solve mode must be -1 (auto), 0 (off) or 1 (on)"};
+        small_mode_ = val;
+        break;
+      case EMPC_OPT_RADIX_SELECT:
+        if (val < 0 || val > 1) throw InvalidArg{"radix selection must be 0 or 1"};
+        if (val && (sizeof(S) != 4 || I_ != 1 || radix_select_smem(d_.N, d_.K) > (size_t)kMaxSmem - 1024))
+          throw InvalidArg{"radix selection needs a single FP32 instance"};
+        use_radix_ = val != 0;
+        break;
       default:
         throw InvalidArg{"unknown option " + std::to_string(opt)};
     }
@@ -1307,6 +1391,11 @@ class Engine final : public EngineBase {
   long long sh_gen0_ = 1;
   bool use_pdl_ = true, pdl_next_ = false, phases_ = false, incremental_ = true;
   int persist_mode_ = -1;  // persistent solve: -1 auto, 0 off, 1 whenever the shape allows
+  int persist_tile_ = 0;   // minimum candidates per persistent CTA (0: one wave over the SMs)
+  int small_mode_ = -1;    // resident single-CTA solve: -1 auto, 0 off, 1 whenever it fits
+  int small_threads_ = 512;
+  bool small_attr_set_ = false;
+  std::string small_desc_;
   bool persist_attr_set_ = false;
   std::vector<PersistVariant<S>> persist_;
   std::string persist_desc_, path_desc_;
@@ -1336,6 +1425,7 @@ class Engine final : public EngineBase {
   double* cws_ = nullptr;   // build workspace
   size_t cws_n_ = 0;
   size_t select_smem_ = 0;
+  bool use_radix_ = false;
   bool have_sched_ = false, have_prob_ = false, r_diag_ = true;
   bool halfk_ = false, halfk_ok_ = std::getenv("EMPC_NO_HALFK") == nullptr;
   std::vector<Slot> slots_;

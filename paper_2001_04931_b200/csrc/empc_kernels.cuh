@@ -901,6 +901,170 @@ __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4 for large candidate sets (FP32 costs, e.g. C4: N = 16384, K = 1024):
+// every CTA finds the K-th smallest 64-bit key (ord(cost) << 32 | row) of the
+// candidate set by an 8-bit radix select over shared memory (<= 8 histogram
+// passes, usually 3), compacts the K elite keys in row order (deterministic
+// block scan), and ranks only its slice of the K elites against the K elite
+// keys (K^2 / CTAs comparisons instead of M^2 / CTAs).  Same result as
+// select_body (unique keys: the stable argsort order); shared memory =
+// radix_select_smem(N).
+
+__host__ __device__ inline size_t radix_select_smem(int N, int K) {
+  return (size_t)N * 8 + (size_t)K * 8 + 256 * 4 + 64 * 4 + 64;
+}
+
+__device__ __forceinline__ void block_exclusive_scan(int& v, int* warp_tot, int& total) {
+  // exclusive prefix sum of v over the block (in thread order), total count
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  total = warp_tot[nw - 1];
+  v = x - v + (warp > 0 ? warp_tot[warp - 1] : 0);
+  __syncthreads();
+}
+
+template <typename S>
+__device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
+                                                  int incremental, int* __restrict__ qcount_in,
+                                                  const void* __restrict__ qlist_in, int* __restrict__ qcount_next,
+                                                  int qcap, const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                                  S* __restrict__ cost_out, int pm) {
+  static_assert(sizeof(S) == 4, "64-bit (ord32, row) keys: FP32 costs");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
+  const int inst = blockIdx.y;
+  const S* c = costs + (size_t)inst * N;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  pdl_wait();
+  int L = 0;
+  bool full = !incremental || K >= N || qcount_in == nullptr;
+  if (!full) {
+    L = qcount_in[inst];
+    full = L > qcap || K + L > N;
+  }
+  const int M = full ? N : K + L;
+  unsigned long long* E = keys + N;                    // [K] elite keys in key-position order
+  int* hist = reinterpret_cast<int*>(E + K);           // [256]
+  int* aux = hist + 256;                               // [64]: warp totals, bucket / remainder broadcast
+  __syncthreads();  // all reads of the count precede its reset below
+  if (blockIdx.x == 0 && tid == 0 && qcount_next != nullptr) qcount_next[inst] = 0;
+  pdl_trigger();
+  const uint32_t* ql = full ? nullptr : reinterpret_cast<const uint32_t*>(qlist_in) + (size_t)inst * qcap * 2;
+  for (int j = tid; j < M; j += nthr) {
+    unsigned long long k;
+    if (j < K || full) k = ((unsigned long long)ord32((float)c[j]) << 32) | (unsigned)j;
+    else k = ((unsigned long long)ql[2 * (j - K)] << 32) | ql[2 * (j - K) + 1];
+    keys[j] = k;
+  }
+  // ---- radix select of the K-th smallest key: prefix / mask of the bucket
+  unsigned long long prefix = 0ull, mask = 0ull;
+  int krem = K;
+  bool done = K >= M;
+  for (int shift = 56; shift >= 0 && !done; shift -= 8) {
+    for (int b = tid; b < 256; b += nthr) hist[b] = 0;
+    __syncthreads();
+    for (int j = tid; j < M; j += nthr) {
+      const unsigned long long k = keys[j];
+      if ((k & mask) == prefix) atomicAdd(&hist[(int)((k >> shift) & 255ull)], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // bucket holding the krem-th key: prefix sums of the 256 bins, 8 per lane
+      int loc[8], s8 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { loc[q] = hist[lane * 8 + q]; s8 += loc[q]; }
+      int inc = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int before = inc - s8;
+      if (before < krem && krem <= inc) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (before < krem && krem <= before + loc[q]) {
+            aux[32] = lane * 8 + q;
+            aux[33] = krem - before;
+            aux[34] = loc[q];
+          }
+          before += loc[q];
+        }
+      }
+    }
+    __syncthreads();
+    const int b = aux[32];
+    krem = aux[33];
+    prefix |= (unsigned long long)b << shift;
+    mask |= 255ull << shift;
+    done = aux[34] == krem;  // the whole bucket is below the threshold
+    __syncthreads();
+  }
+  // elites: keys below the bucket, plus the bucket when it is taken whole
+  // (the loop ends with exactly K keys <= thr)
+  const unsigned long long thr = K >= M ? ~0ull : (prefix | ~mask);
+  // ---- deterministic compaction of the K elite keys (block scan in key-position order)
+  const int chunk = (M + nthr - 1) / nthr;
+  const int j0 = min(M, tid * chunk), j1 = min(M, j0 + chunk);
+  int cnt = 0;
+  for (int j = j0; j < j1; ++j) cnt += keys[j] <= thr ? 1 : 0;
+  int total;
+  block_exclusive_scan(cnt, aux, total);
+  for (int j = j0; j < j1; ++j)
+    if (keys[j] <= thr) E[cnt++] = keys[j];
+  __syncthreads();
+  // ---- rank this CTA's slice of the elites (K keys, unique)
+  const int ne = min(K, total);
+  const int per = (ne + gridDim.x - 1) / gridDim.x;
+  const int e0 = blockIdx.x * per, e1 = min(ne, e0 + per);
+  for (int e = e0 + warp; e < e1; e += nwarps) {
+    const unsigned long long ke = E[e];
+    int r = 0;
+    for (int j = lane; j < ne; j += 32) r += E[j] < ke ? 1 : 0;
+    r = __reduce_add_sync(0xFFFFFFFFu, r);
+    const int re = (int)(uint32_t)ke;
+    if (lane == 0) elite_idx[(size_t)inst * K + r] = re;
+    if (pop_out != nullptr) {
+      const S* from = pop_in + ((size_t)inst * N + re) * pm;
+      S* to = pop_out + ((size_t)inst * N + r) * pm;
+      for (int g = lane; g < pm; g += 32) to[g] = from[g];
+      if (lane == 0) cost_out[(size_t)inst * N + r] = c[re];
+    }
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(1024) select_radix_kernel(const S* __restrict__ costs, int N, int K,
+                                                            int* __restrict__ elite_idx, int incremental,
+                                                            int* __restrict__ qcount_in,
+                                                            const void* __restrict__ qlist_in,
+                                                            int* __restrict__ qcount_next, int qcap,
+                                                            const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                                            S* __restrict__ cost_out, int pm) {
+  if constexpr (sizeof(S) == 4)
+    select_radix_body<S>(costs, N, K, elite_idx, incremental, qcount_in, qlist_in, qcount_next, qcap, pop_in, pop_out,
+                         cost_out, pm);
+}
+
 template <typename S>
 __global__ void __launch_bounds__(256) select_kernel(const S* __restrict__ costs, int N, int K,
                                                      int* __restrict__ elite_idx, int incremental,

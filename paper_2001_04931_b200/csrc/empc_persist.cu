@@ -29,7 +29,10 @@ std::vector<PersistVariant<float>> persist_variants<float>() {
           PKH(48, 2, 4, true, 2), PKH(48, 1, 4, true, 1), PKH(32, 2, 4, true, 2),
           PKW(48, 3, 4, true, 2, false, 256), PKW(48, 3, 4, true, 2, true, 384),
           // one warp = two candidate groups of 16 lanes x 3 rows, no split-K shuffle
-          PKW(48, 3, 1, true, 1, true, 448), PKW(48, 3, 2, true, 1, true, 384)};
+          PKW(48, 3, 1, true, 1, true, 448), PKW(48, 3, 2, true, 1, true, 384),
+          // small states (C1, C2): warp-synchronous groups of NRG lanes, several per warp
+          PKW(4, 1, 4, true, 1, false, 512), PKW(4, 1, 2, true, 1, false, 512),
+          PKW(12, 3, 4, true, 1, false, 512), PKW(12, 3, 2, true, 1, false, 512)};
 }
 
 template <>

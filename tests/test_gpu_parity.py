@@ -550,3 +550,23 @@ def test_persistent_half_k_solve_matches_oracle(cfg):
     pr2 = O.Problem.from_spec(spec2)
     np.testing.assert_allclose(res2.population.costs, O.rollout_costs(res2.population.candidates, pr2, x0s[0]),
                                rtol=RTOL32)
+
+
+def test_radix_selection_solve_equals_counting_selection():
+    """Large single populations (C4-sized N) select by radix select + ranking
+    of the K elites; the whole solve must equal the rank-by-counting path bit
+    for bit (same stable order of unique (cost, row) keys)."""
+    from paper_2001_04931_b200 import workloads as W
+
+    spec, x0 = W.nlink_problem(6, 50, 0)
+    sched = P.KnotSchedule(50, 3)
+    st = P.EmpcSettings(num_sims=16384, num_parents=1024, generations=4, seed=5)
+    ctx = P.empc._spec_context(spec, sched, st)
+    out = []
+    for radix in (1, 0):
+        ctx.h.set_option(nat.EMPC_OPT_RADIX_SELECT, radix)
+        r = P.solve_empc(spec, sched, st, x0)
+        out.append((r.population.candidates, r.population.costs, r.best))
+    ctx.h.set_option(nat.EMPC_OPT_RADIX_SELECT, 1)
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)

@@ -1,2 +1,2 @@
-for G in 2 3 10; do timeout 120 python tools/dbg_ws.py $G | tail -1; done
-timeout 900 python -m pytest tests -q -m gpu --timeout 300 2>&1 | tail -3
+python tools/sweep.py c1 '' 'EMPC_SMALL_THREADS=128' 'EMPC_SMALL_THREADS=256'
+timeout 900 python -m pytest tests -q -m gpu --timeout 400 2>&1 | tail -2
