@@ -153,9 +153,11 @@ def check(rc: int, handle=None):
 _keep = collections.deque(maxlen=512)
 
 
-def dptr(a: np.ndarray):
+def dptr(a: np.ndarray) -> int:
+    """Address of a C-contiguous array for a void* argument (ctypes converts
+    the int); the array is kept alive for the next few hundred conversions."""
     _keep.append(a)
-    return C.c_void_p(a.ctypes.data)
+    return a.ctypes.data
 
 
 iptr = u8ptr = u32ptr = dptr

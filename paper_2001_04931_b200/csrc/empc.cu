@@ -180,8 +180,10 @@ class Engine final : public EngineBase {
     {
       const char* e = std::getenv("EMPC_RADIX_SELECT");
       const int min_n = e ? std::atoi(e) : 8192;
-      use_radix_ = sizeof(S) == 4 && I_ == 1 && min_n > 0 && d_.N >= min_n &&
+      radix_min_n_ = min_n > 0 ? min_n : (1 << 30);
+      use_radix_ = sizeof(S) == 4 && I_ == 1 && d_.N >= radix_min_n_ &&
                    radix_select_smem(d_.N, d_.K) <= (size_t)kMaxSmem - 1024;
+      radix_persist_ok_ = min_n > 0;
       CK(cudaFuncSetAttribute(select_radix_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
     }
     for (auto& v : variants_) CK(cudaFuncSetAttribute(v.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -532,8 +534,9 @@ class Engine final : public EngineBase {
       if (d_.NP <= 8) {
         pref[0] = find(1, 4, true, 1);
       } else if (d_.NP <= 16) {
-        pref[0] = find(2, 2, true, 1);
-        pref[1] = find(1, 4, true, 1);
+        pref[0] = I_ == 1 ? find(3, 2, true, 1, true) : nullptr;  // NP = 12 (C2): persistent WS
+        pref[1] = find(2, 2, true, 1);
+        pref[2] = find(1, 4, true, 1);
       } else if (d_.NP == 48 && I_ == 1) {
         // warp-synchronous candidate groups + helper warps that draw the
         // next generation during the recursion (persistent solve, C3)
@@ -668,6 +671,13 @@ class Engine final : public EngineBase {
     ++launches_;
   }
 
+  // the persistent solve selects by radix select for FP32 unless disabled
+  // (EMPC_OPT_RADIX_SELECT = 0 forces rank-by-counting everywhere)
+  bool persist_radix() const { return sizeof(S) == 4 && (use_radix_ || (radix_persist_ok_ && d_.N >= 2048)); }
+  size_t persist_select_smem() const {
+    return persist_radix() ? std::max(select_smem_, radix_select_smem(d_.N, d_.K)) : select_smem_;
+  }
+
   // Persistent cooperative path (single instance, default variant, every
   // tile co-resident): the whole run is one launch.  Returns false when the
   // configuration does not qualify and the per-generation launches are used.
@@ -677,9 +687,11 @@ class Engine final : public EngineBase {
     // small problems (n <= 16: C1, C2) run faster as per-generation launches
     // with several small CTAs per SM (profiles/bench_c1/c2): persistent only
     // from NP = 24 unless forced (EMPC_OPT_PERSISTENT = 1)
-    if (persist_mode_ == 0 || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K ||
-        (d_.NP < 24 && forced_ < 0 && persist_mode_ < 1))
+    if (persist_mode_ == 0 || scorer_ != 0 || I_ != 1 || cps_ > 0 || (!r.init && !r.rescore) || d_.N == d_.K)
       return false;
+    // small states run persistent only with the warp-synchronous variants
+    // (C2: 0.176 vs 0.217 ms per-generation launches)
+    if (d_.NP < 24 && forced_ < 0 && persist_mode_ < 1 && !pick().ws) return false;
     const Variant<S>& v = pick();
     if (v.tc) return false;
     const PersistVariant<S>* pv = nullptr;
@@ -708,7 +720,7 @@ class Engine final : public EngineBase {
     if (v.ws) threads = std::max(threads, std::min(pv->maxt, ws_threads_) / 32 * 32);
     if (threads > pv->maxt) return false;
     const size_t smem =
-        smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq, select_smem_).total;
+        smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq, persist_select_smem()).total;
     if (smem > (size_t)kMaxSmem - 1024) return false;
     if (!persist_attr_set_) {
       for (auto& p : persist_)
@@ -732,15 +744,18 @@ class Engine final : public EngineBase {
     a.pop_in = pop_[0]; a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
     a.elite_idx = elite_; a.run = run_d_;
     a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
-    if (phases_ && (size_t)grid * 16 <= dbg_n_) {
-      CK(cudaMemsetAsync(dbg_, 0, (size_t)grid * 16 * 8, stream_));
+    if (phases_ && (size_t)grid * 16 + 32 <= dbg_n_) {
+      CK(cudaMemsetAsync(dbg_, 0, ((size_t)grid * 16 + 32) * 8, stream_));
       a.dbg = dbg_;
       dbg_ctas_ = grid;
     }
     P.evolves = r.evolves;
     P.tile_evolve = Le.tile;
     P.incremental = incremental_ ? 1 : 0;
-    P.scratch = select_smem_;
+    P.scratch = persist_select_smem();
+    P.radix = persist_radix() ? 1 : 0;
+    P.dbg_gen = -1;
+    if (const char* e = std::getenv("EMPC_PHASES_GEN")) P.dbg_gen = std::atoi(e);
     P.pop[0] = pop_[0]; P.pop[1] = pop_[1];
     P.cost[0] = cost_[0]; P.cost[1] = cost_[1];
     P.qcount = qcount_;
@@ -929,7 +944,7 @@ class Engine final : public EngineBase {
   GKey gkey(const empc_run_args& r, bool io) const {
     return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io, tc_mode_,
                            halfk_, persist_mode_ + 4 * persist_tile_ + (small_mode_ + 1) * (1 << 24), halfk_ok_,
-                           (incremental_ ? 1 : 0) | (use_radix_ ? 2 : 0));
+                           (incremental_ ? 1 : 0) | (use_radix_ ? 2 : 0) | (radix_persist_ok_ ? 4 : 0));
   }
 
   // One graph per run shape.  io = true also captures the staging H2D copies
@@ -1154,6 +1169,14 @@ class Engine final : public EngineBase {
       }
       if (cnt) std::fprintf(stderr, "persist(us, mean over %d CTAs): sync_before_select=%.2f select=%.2f sync_after=%.2f\n",
                             cnt, w1 / cnt, w2 / cnt, w3 / cnt);
+      if (cnt) {  // per-generation timeline of the persistent solve (CTA 0)
+        std::vector<unsigned long long> gt(32);
+        CK(cudaMemcpy(gt.data(), dbg_ + (size_t)dbg_ctas_ * 16, 32 * 8, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "persist timeline (us from kernel start): init_rollout_end=%.2f", (gt[1] - gt[0]) * 1e-3);
+        for (int g = 2; g < 30 && gt[g] > gt[0]; ++g) std::fprintf(stderr, " gen%d_end=%.2f", g - 1, (gt[g] - gt[0]) * 1e-3);
+        if (gt[31] > gt[0]) std::fprintf(stderr, " end=%.2f", (gt[31] - gt[0]) * 1e-3);
+        std::fprintf(stderr, "\n");
+      }
     }
   }
 
@@ -1321,6 +1344,7 @@ class Engine final : public EngineBase {
         if (val && (sizeof(S) != 4 || I_ != 1 || radix_select_smem(d_.N, d_.K) > (size_t)kMaxSmem - 1024))
           throw InvalidArg{"radix selection needs a single FP32 instance"};
         use_radix_ = val != 0;
+        radix_persist_ok_ = val != 0;
         break;
       default:
         throw InvalidArg{"unknown option " + std::to_string(opt)};
@@ -1426,6 +1450,8 @@ class Engine final : public EngineBase {
   size_t cws_n_ = 0;
   size_t select_smem_ = 0;
   bool use_radix_ = false;
+  bool radix_persist_ok_ = true;  // cleared by EMPC_OPT_RADIX_SELECT = 0
+  int radix_min_n_ = 8192;
   bool have_sched_ = false, have_prob_ = false, r_diag_ = true;
   bool halfk_ = false, halfk_ok_ = std::getenv("EMPC_NO_HALFK") == nullptr;
   std::vector<Slot> slots_;

@@ -982,9 +982,17 @@ __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, i
   for (int shift = 56; shift >= 0 && !done; shift -= 8) {
     for (int b = tid; b < 256; b += nthr) hist[b] = 0;
     __syncthreads();
-    for (int j = tid; j < M; j += nthr) {
-      const unsigned long long k = keys[j];
-      if ((k & mask) == prefix) atomicAdd(&hist[(int)((k >> shift) & 255ull)], 1);
+    // warp-aggregated histogram: costs of a converging population share
+    // their top bytes, so plain shared atomics would serialise on one bin
+    for (int j0 = warp * 32; j0 < M; j0 += nwarps * 32) {
+      const int j = j0 + lane;
+      int bin = 256;
+      if (j < M) {
+        const unsigned long long k = keys[j];
+        if ((k & mask) == prefix) bin = (int)((k >> shift) & 255ull);
+      }
+      const unsigned same = __match_any_sync(0xFFFFFFFFu, bin);
+      if (bin < 256 && lane == __ffs(same) - 1) atomicAdd(&hist[bin], __popc(same));
     }
     __syncthreads();
     if (warp == 0) {
@@ -1313,6 +1321,8 @@ struct PersistArgs {
   int* elite;         // elite_idx (written by the selection)
   double* out;
   int predraw;        // WS variant with helper warps: next-generation draws during the recursion
+  int radix;          // selection by radix select (FP32)
+  int dbg_gen;        // EMPC_PHASES: evolve whose phases are recorded (-1: every one, the last wins)
   // injected draws of the evolves (parity mode; NULL: in-kernel Philox):
   // evolve g reads parents + g (N-K) 2, masks / noise + g (N-K) p m
   const int* inj_parents;
@@ -1334,20 +1344,43 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   a.draw_evolve = 0;
   a.draw_tile0 = dt0;
   a.draw_cnt = min(P.tile_evolve, nc - dt0);
+  // phase timers (EMPC_PHASES): CTA 0 stamps the start, the end of the init
+  // rollout and the end of every generation (after `gridDim.x * 16` slots)
+  unsigned long long* gt = (a.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + gridDim.x * 16 : nullptr;
+  if (gt) gt[0] = gtimer();
   rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(a, true, P.scratch);
+  if (gt) gt[1] = gtimer();
   int cur = 0;
   for (int g = 0; g < P.evolves; ++g) {
+    if (gt && g > 0 && g + 1 < 30) gt[g + 1] = gtimer();
     EMPC_MARK(13)
     grid.sync();
     EMPC_MARK(14)
     const int inc = (g > 0 && P.incremental) ? 1 : 0;
-    select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
-                   (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
-                   P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+    if constexpr (sizeof(S) == 4) {
+      if (P.radix && !inc) {
+        // the first selection ranks all N candidates (35 us by counting at
+        // C3): radix select of the K-th key + ranking of the K elites only.
+        // Later (incremental) sets are small enough for rank-by-counting,
+        // which needs fewer passes and barriers
+        select_radix_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+                             (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap,
+                             P.pop[cur], P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+      } else {
+        select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+                       (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
+                       P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+      }
+    } else {
+      select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+                     (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
+                     P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+    }
     EMPC_MARK(15)
     grid.sync();
     RolloutArgs<S> b = a;
     b.mode = P.inj_parents != nullptr ? kBreedInject : kBreedPhilox;
+    if (P.dbg_gen >= 0) b.dbg = g == P.dbg_gen ? a.dbg : nullptr;  // phase marks of one chosen evolve
     if (P.inj_parents != nullptr) {
       const size_t per = (size_t)(N - K) * pm;
       b.inj_parents = P.inj_parents + (size_t)g * (N - K) * 2;
@@ -1375,8 +1408,10 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(b, false, P.scratch);
     cur ^= 1;
   }
+  if (gt && P.evolves > 0 && P.evolves + 1 < 30) gt[P.evolves + 1] = gtimer();
   grid.sync();
   if (blockIdx.x == 0) finalize_body<S>(P.pop[cur], P.cost[cur], N, a.d.m, pm, P.out, 0);
+  if (gt) gt[31] = gtimer();
 }
 
 }  // namespace empc

@@ -200,11 +200,20 @@ class _Context:
         return s
 
     def set_problems(self, probs):
-        """probs: dict of stacked FP64 arrays (instances leading)."""
-        a = [nat.f64(probs[k]) for k in ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")]
-        self.h.call("empc_set_problems", 0, self.dims.instances, *[nat.dptr(x) for x in a])
+        """probs: dict of stacked FP64 arrays (instances leading).  Packed into
+        one contiguous FP64 buffer (one conversion, nine offsets) -- the
+        per-array Python overhead dominated the end-to-end latency of C1-C3."""
+        parts = [np.ravel(probs[k]) for k in _PROBLEM_KEYS]
+        buf = np.concatenate(parts).astype(np.float64, copy=False)
+        base = nat.dptr(buf)
+        ptrs, off = [], 0
+        for x in parts:
+            ptrs.append(base + 8 * off)
+            off += x.size
+        self.h.call("empc_set_problems", 0, self.dims.instances, *ptrs)
 
 
+_PROBLEM_KEYS = ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")
 _contexts: dict = {}
 
 
@@ -291,6 +300,7 @@ def _run(ctx: _Context, settings, x0, sigma, *, init, rescore, evolves, gen0, sl
     best = np.empty((d.instances, d.p, d.m))
     bc = np.empty(d.instances)
     bi = np.empty(d.instances, np.int32)
+    # (fresh output arrays per call: results stay valid after the next solve)
     a.init, a.rescore, a.evolves = int(init), int(rescore), int(evolves)
     a.slot_in = slot_in.id if slot_in is not None else -1
     a.slot_out = out_slot.id

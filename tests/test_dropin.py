@@ -30,8 +30,9 @@ def _array_at(ptr):
     """The numpy array behind a pointer handed to the ABI (kept alive by nat._keep)."""
     addr = ptr.value if isinstance(ptr, C.c_void_p) else ptr
     for a in reversed(nat._keep):
-        if a.ctypes.data == addr:
-            return a
+        base = a.ctypes.data
+        if base <= addr < base + max(a.nbytes, 1):  # the array or a packed part of it
+            return a.reshape(-1)[(addr - base) // a.itemsize:]
     raise KeyError(addr)
 
 
@@ -64,9 +65,8 @@ class FakeHandle:
             rec["x0"] = _array_at(a.x0).copy()
             rec["sigma"] = _array_at(a.sigma).copy()
             FakeHandle.log.append((name, rec))
-            for ptr, shape in ((a.u_out, (d.instances, d.m)), (a.best_out, (d.instances, d.p, d.m)),
-                               (a.best_cost, (d.instances,))):
-                _array_at(C.c_void_p(ptr))[...] = 1.0
+            for ptr in (a.u_out, a.best_out, a.best_cost):
+                _array_at(ptr)[...] = 1.0
         else:
             FakeHandle.log.append((name, args))
 
