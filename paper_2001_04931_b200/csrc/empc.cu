@@ -160,6 +160,7 @@ class Engine final : public EngineBase {
     CK(cudaMalloc(&idx1_, sizeof(int) * d_.T));
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
     CK(cudaMalloc(&seg_, sizeof(int) * d_.T));
+    CK(cudaMalloc(&amin_d_, sizeof(unsigned long long)));
     if (const char* v = std::getenv("EMPC_STAGGER")) stagger_ = std::atoi(v);
     if (const char* v = std::getenv("EMPC_WS_THREADS")) ws_threads_ = std::atoi(v);
     if (const char* v = std::getenv("EMPC_PERSIST")) persist_mode_ = std::atoi(v);
@@ -200,7 +201,7 @@ class Engine final : public EngineBase {
     cudaFreeHost(stage_prob_h_); cudaFreeHost(stage_state_h_);
     for (int b = 0; b < 2; ++b) { cudaFree(pop_[b]); cudaFree(cost_[b]); }
     cudaFree(elite_); cudaFree(qcount_); cudaFree(qlist_); cudaFree(out_d_); cudaFreeHost(out_h_);
-    cudaFree(idx1_); cudaFree(idx2_); cudaFree(seg_); cudaFree(cw_); cudaFree(G_);
+    cudaFree(idx1_); cudaFree(idx2_); cudaFree(seg_); cudaFree(cw_); cudaFree(G_); cudaFree(amin_d_);
     cudaFree(W64_); cudaFree(G64_);
     if (cond_) cudaFree(cond_);
     if (cws_) cudaFree(cws_);
@@ -755,6 +756,7 @@ class Engine final : public EngineBase {
     P.scratch = persist_select_smem();
     P.radix = persist_radix() ? 1 : 0;
     P.dbg_gen = -1;
+    P.amin = sizeof(S) == 4 ? amin_d_ : nullptr;
     if (const char* e = std::getenv("EMPC_PHASES_GEN")) P.dbg_gen = std::atoi(e);
     P.pop[0] = pop_[0]; P.pop[1] = pop_[1];
     P.cost[0] = cost_[0]; P.cost[1] = cost_[1];
@@ -1438,6 +1440,7 @@ class Engine final : public EngineBase {
   double *out_d_ = nullptr, *out_h_ = nullptr;
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
+  unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key
   int stagger_ = 0;       // WS recursion phase offset (cycles), EMPC_STAGGER
   bool predraw_ok_ = std::getenv("EMPC_NO_PREDRAW") == nullptr;
   int ws_threads_ = 352;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)

@@ -86,6 +86,7 @@ struct RolloutArgs {
   int draw_next;            // helper warps draw evolve `draw_evolve`'s tile during the recursion
   int draw_evolve;
   int draw_tile0, draw_cnt; // that tile (children [draw_tile0, draw_tile0 + draw_cnt))
+  unsigned long long* amin; // last generation of the persistent solve: argmin key of the population
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -140,6 +141,14 @@ __host__ __device__ inline SmemPlan smem_plan(int NP, int m, int T, int p, int t
 }
 
 __device__ __forceinline__ uint32_t ord_key(float c) { return ord32(c); }
+// numpy argmin order as one 64-bit key: NaN first, then by value, then row
+__device__ __forceinline__ unsigned long long amin_key(float c, int row) {
+  return ((unsigned long long)((c != c) ? 0u : ord32(c)) << 32) | (unsigned)row;
+}
+__device__ __forceinline__ unsigned long long amin_key(double c, int row) {
+  // FP64: the top 32 bits of the orderable key, ties resolved by the full scan
+  return ((unsigned long long)((c != c) ? 0u : (uint32_t)(ord64(c) >> 32)) << 32) | (unsigned)row;
+}
 __device__ __forceinline__ uint64_t ord_key(double c) { return ord64(c); }
 
 // Programmatic dependent launch: wait for the producer grid (no-op when the
@@ -785,6 +794,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     const S cost = c0s + s;
     const int row = a.row0 + tile0 + c;
     a.cost_out[pop_base + row] = cost;
+    if (a.amin != nullptr) atomicMin(a.amin, amin_key(cost, row));  // last generation: distributed argmin
     if (qual) {
       const OT kc = ord_key(cost);
       if (kc < tau) {
@@ -1323,6 +1333,7 @@ struct PersistArgs {
   int predraw;        // WS variant with helper warps: next-generation draws during the recursion
   int radix;          // selection by radix select (FP32)
   int dbg_gen;        // EMPC_PHASES: evolve whose phases are recorded (-1: every one, the last wins)
+  unsigned long long* amin;  // distributed argmin key (FP32), NULL: CTA 0 scans the population
   // injected draws of the evolves (parity mode; NULL: in-kernel Philox):
   // evolve g reads parents + g (N-K) 2, masks / noise + g (N-K) p m
   const int* inj_parents;
@@ -1348,6 +1359,12 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   // rollout and the end of every generation (after `gridDim.x * 16` slots)
   unsigned long long* gt = (a.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + gridDim.x * 16 : nullptr;
   if (gt) gt[0] = gtimer();
+  // distributed argmin of the final population (FP32, at least one evolve):
+  // every CTA folds its rows of the last generation into one 64-bit key;
+  // reset here, first folded after two grid barriers
+  const bool dist_amin = sizeof(S) == 4 && P.amin != nullptr;
+  if (dist_amin && blockIdx.x == 0 && threadIdx.x == 0) *P.amin = ~0ull;
+  a.amin = nullptr;
   rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(a, true, P.scratch);
   if (gt) gt[1] = gtimer();
   int cur = 0;
@@ -1390,6 +1407,7 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     }
     b.nc = N - K;
     b.row0 = K;
+    b.amin = (dist_amin && g + 1 == P.evolves) ? P.amin : nullptr;
     b.tile = P.tile_evolve;
     b.evolve = g;
     b.copy_elites = 0;
@@ -1409,8 +1427,29 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     cur ^= 1;
   }
   if (gt && P.evolves > 0 && P.evolves + 1 < 30) gt[P.evolves + 1] = gtimer();
+  if (dist_amin && P.evolves > 0) {
+    // the elite rows [0, K) of the final population, a slice per CTA
+    const int per = (K + gridDim.x - 1) / gridDim.x;
+    for (int r = blockIdx.x * per + threadIdx.x; r < min(K, (int)(blockIdx.x + 1) * per); r += blockDim.x)
+      atomicMin(P.amin, amin_key(P.cost[cur][r], r));
+  }
   grid.sync();
-  if (blockIdx.x == 0) finalize_body<S>(P.pop[cur], P.cost[cur], N, a.d.m, pm, P.out, 0);
+  if (blockIdx.x == 0) {
+    if (dist_amin && P.evolves > 0) {
+      const int best = (int)(uint32_t)*reinterpret_cast<volatile unsigned long long*>(P.amin);
+      const S* bc = P.pop[cur] + (size_t)best * pm;
+      for (int q = threadIdx.x; q < pm; q += blockDim.x) {
+        P.out[a.d.m + q] = (double)bc[q];
+        if (q < a.d.m) P.out[q] = (double)bc[q];  // u = first knot (K/empc.py:236)
+      }
+      if (threadIdx.x == 0) {
+        P.out[a.d.m + pm] = (double)P.cost[cur][best];
+        P.out[a.d.m + pm + 1] = (double)best;
+      }
+    } else {
+      finalize_body<S>(P.pop[cur], P.cost[cur], N, a.d.m, pm, P.out, 0);
+    }
+  }
   if (gt) gt[31] = gtimer();
 }
 
