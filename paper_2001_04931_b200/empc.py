@@ -175,8 +175,28 @@ class _Context:
             self.h.call("empc_pop_alloc", nat.C.byref(v))
             self.free.append(v.value)
         self.args = nat.empc_run_args()
+        self._spec_arrays = self._spec_ptrs = self._spec_conv = None
+        self._spec_copied = []
+        self._io = None
         self.scorer = 0
         self.tc = -1
+
+    def io_buffers(self):
+        """Per-context input / output arrays of empc_run with their pointers
+        stored in the argument struct once (the pointer extraction of fresh
+        arrays dominated the host time of a sub-ms solve)."""
+        if self._io is None:
+            d = self.dims
+            io = {"x0": np.zeros((d.instances, d.n)), "sigma": np.zeros((d.instances, d.m)),
+                  "u": np.zeros((d.instances, d.m)), "best": np.zeros((d.instances, d.p, d.m)),
+                  "bc": np.zeros(d.instances), "bi": np.zeros(d.instances, np.int32)}
+            a = self.args
+            a.x0, a.sigma = io["x0"].ctypes.data, io["sigma"].ctypes.data
+            a.u_out, a.best_out = io["u"].ctypes.data, io["best"].ctypes.data
+            a.best_cost, a.best_index = io["bc"].ctypes.data, io["bi"].ctypes.data
+            self._io = io
+            self.args_ref = nat.C.byref(a)
+        return self._io
 
     def set_scorer(self, code: int):
         if code != self.scorer:
@@ -199,10 +219,41 @@ class _Context:
         s = _Slot(sid, self.free)
         return s
 
+    def set_spec(self, spec):
+        """Stage one spec (instances == 1).  The nine array pointers are
+        memoised on the identity of the spec's array objects -- the library
+        copies the CURRENT contents at every call, so an array mutated in
+        place is still staged correctly; only the pointer extraction is
+        skipped (it dominated the host time of a C3 solve)."""
+        mdl = spec.model
+        arrs = (mdl.Ad, mdl.Bd, mdl.wd, spec.Q, spec.R, spec.x_goal, spec.u_goal, spec.u_min, spec.u_max)
+        last = self._spec_arrays
+        if last is not None and all(a is b for a, b in zip(arrs, last)):
+            # same array objects: refresh the converted copies of the ones
+            # that are not contiguous FP64 (in-place edits stay visible)
+            for i in self._spec_copied:
+                np.copyto(self._spec_conv[i], arrs[i])
+            self.h.call("empc_set_problems", 0, 1, *self._spec_ptrs)
+            return
+        d = self.dims
+        n, m = d.n, d.m
+        shapes = ((n, n), (n, m), (n,), (n, n), (m, m), (n,), (m,), (m,), (m,))
+        conv = []
+        for a, sh in zip(arrs, shapes):
+            c = np.asarray(a, dtype=np.float64)
+            if c.shape != sh:
+                c = np.broadcast_to(c, sh)
+            conv.append(np.ascontiguousarray(c))
+        ptrs = [nat.dptr(c) for c in conv]
+        self.h.call("empc_set_problems", 0, 1, *ptrs)
+        self._spec_arrays, self._spec_ptrs, self._spec_conv = arrs, ptrs, conv
+        self._spec_copied = [i for i, (c, a) in enumerate(zip(conv, arrs)) if c is not a]
+
     def set_problems(self, probs):
         """probs: dict of stacked FP64 arrays (instances leading).  Packed into
         one contiguous FP64 buffer (one conversion, nine offsets) -- the
         per-array Python overhead dominated the end-to-end latency of C1-C3."""
+        self._spec_arrays = self._spec_ptrs = None
         parts = [np.ravel(probs[k]) for k in _PROBLEM_KEYS]
         buf = np.concatenate(parts).astype(np.float64, copy=False)
         base = nat.dptr(buf)
@@ -228,6 +279,23 @@ def _context(n, m, T, p, N, K, instances, dense_q, precision) -> _Context:
 def _is_diag(Q) -> bool:
     """The reference's diagonal-Q test (K/empc.py:114)."""
     return int(np.count_nonzero(Q)) == int(np.count_nonzero(np.diagonal(Q)))
+
+
+def _spec_dense_q(spec) -> bool:
+    """Dense-Q test of the spec's Q, memoised on the Q array object (the
+    reference tests the nonzero pattern, K/empc.py:114)."""
+    Q = spec.Q
+    hit = _dense_memo.get(id(Q))
+    if hit is not None and hit[0] is Q:
+        return hit[1]
+    d = not _is_diag(Q)
+    if len(_dense_memo) > 64:
+        _dense_memo.clear()
+    _dense_memo[id(Q)] = (Q, d)
+    return d
+
+
+_dense_memo: dict = {}
 
 
 def _problem_arrays(spec):
@@ -269,9 +337,10 @@ def _scorer_code(scorer: str, spec=None) -> int:
 def _spec_context(spec, sched, settings, instances=1) -> _Context:
     _check_sched(spec, sched)
     n, m = spec.model.Ad.shape[0], spec.model.Bd.shape[1]
-    ctx = _context(n, m, spec.T, sched.p, settings.num_sims, settings.num_parents, instances, not _is_diag(spec.Q),
+    dense = _spec_dense_q(spec)
+    ctx = _context(n, m, spec.T, sched.p, settings.num_sims, settings.num_parents, instances, dense,
                    getattr(settings, "precision", "fp32"))
-    ctx.set_problems(_problem_arrays(spec))
+    ctx.set_spec(spec)
     ctx.set_scorer(_scorer_code(getattr(settings, "scorer", "rollout"), spec))
     ctx.set_tensor_cores(getattr(settings, "tensor_cores", "auto"))
     return ctx
@@ -293,14 +362,12 @@ def _device_population(ctx: _Context, pop: Population) -> _Slot:
 def _run(ctx: _Context, settings, x0, sigma, *, init, rescore, evolves, gen0, slot_in=None, inject=None):
     d = ctx.dims
     a = ctx.args
+    io = ctx.io_buffers()
     out_slot = ctx.slot()
-    x0 = nat.f64(x0)
-    sigma = nat.f64(sigma)
-    u = np.empty((d.instances, d.m))
-    best = np.empty((d.instances, d.p, d.m))
-    bc = np.empty(d.instances)
-    bi = np.empty(d.instances, np.int32)
-    # (fresh output arrays per call: results stay valid after the next solve)
+    # inputs into the context's staging arrays (pointers cached once), outputs
+    # read back from its result arrays and returned as fresh copies
+    np.copyto(io["x0"], np.reshape(x0, io["x0"].shape))
+    np.copyto(io["sigma"], np.reshape(sigma, io["sigma"].shape))
     a.init, a.rescore, a.evolves = int(init), int(rescore), int(evolves)
     a.slot_in = slot_in.id if slot_in is not None else -1
     a.slot_out = out_slot.id
@@ -308,11 +375,9 @@ def _run(ctx: _Context, settings, x0, sigma, *, init, rescore, evolves, gen0, sl
     a.seed = int(settings.seed) & 0xFFFFFFFFFFFFFFFF
     a.mutation_prob = float(settings.mutation_prob)
     a.crossover_prob = float(settings.crossover_prob)
-    a.x0, a.sigma = nat.dptr(x0), nat.dptr(sigma)
     a.inject = nat.C.pointer(inject) if inject is not None else None
-    a.u_out, a.best_out, a.best_cost, a.best_index = nat.dptr(u), nat.dptr(best), nat.dptr(bc), nat.iptr(bi)
-    ctx.h.call("empc_run", nat.C.byref(a))
-    return out_slot, u, best, bc, bi
+    ctx.h.call("empc_run", ctx.args_ref)
+    return out_slot, io["u"].copy(), io["best"].copy(), io["bc"].copy(), io["bi"].copy()
 
 
 # ---------------------------------------------------------------------------

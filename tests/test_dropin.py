@@ -29,7 +29,8 @@ pytestmark = pytest.mark.skipif(not os.path.isdir(REF), reason="reference packag
 def _array_at(ptr):
     """The numpy array behind a pointer handed to the ABI (kept alive by nat._keep)."""
     addr = ptr.value if isinstance(ptr, C.c_void_p) else ptr
-    for a in reversed(nat._keep):
+    io = [a for ctx in E._contexts.values() if getattr(ctx, "_io", None) for a in ctx._io.values()]
+    for a in list(reversed(nat._keep)) + io:
         base = a.ctypes.data
         if base <= addr < base + max(a.nbytes, 1):  # the array or a packed part of it
             return a.reshape(-1)[(addr - base) // a.itemsize:]
