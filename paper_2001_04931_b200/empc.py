@@ -250,18 +250,12 @@ class _Context:
         self._spec_copied = [i for i, (c, a) in enumerate(zip(conv, arrs)) if c is not a]
 
     def set_problems(self, probs):
-        """probs: dict of stacked FP64 arrays (instances leading).  Packed into
-        one contiguous FP64 buffer (one conversion, nine offsets) -- the
-        per-array Python overhead dominated the end-to-end latency of C1-C3."""
+        """probs: dict of stacked FP64 arrays (instances leading); the library
+        interleaves them into its pinned staging block (multi-threaded for
+        large batches)."""
         self._spec_arrays = self._spec_ptrs = None
-        parts = [np.ravel(probs[k]) for k in _PROBLEM_KEYS]
-        buf = np.concatenate(parts).astype(np.float64, copy=False)
-        base = nat.dptr(buf)
-        ptrs, off = [], 0
-        for x in parts:
-            ptrs.append(base + 8 * off)
-            off += x.size
-        self.h.call("empc_set_problems", 0, self.dims.instances, *ptrs)
+        a = [nat.f64(probs[k]) for k in _PROBLEM_KEYS]
+        self.h.call("empc_set_problems", 0, self.dims.instances, *[nat.dptr(x) for x in a])
 
 
 _PROBLEM_KEYS = ("Ad", "Bd", "wd", "Q", "R", "x_goal", "u_goal", "u_min", "u_max")

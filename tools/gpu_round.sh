@@ -1,21 +1,21 @@
-# Round measurement: tests, bench lines for every config, reference arm, ncu evidence.
+# Round measurement: tests, bench lines for every config, reference arms, ncu
+# evidence; everything lands in gpurun_out/r02/ (copied to profiles/ by hand).
 set -x
-./tools/tf32_peak > gpurun_out/tf32_peak.json
-timeout 900 python -m pytest tests/ -q -m gpu --timeout 300 2>&1 | tail -3
-timeout 600 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; tail -3 gpurun_out/bench_c3.err
-timeout 600 python bench.py --impl reference --steps 20 --warmup 2 > gpurun_out/bench_ref_c3.json 2> gpurun_out/bench_ref.err
-for c in c1 c2; do timeout 300 python bench.py --config $c --steps 100 --warmup 10 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
-timeout 900 python bench.py --config c4 --steps 10 --warmup 3 --cpu-sample-s 20 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-timeout 900 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline --tensor-cores off > gpurun_out/bench_c4_ffma.json 2> gpurun_out/bench_c4_ffma.err
-timeout 1200 python bench.py --config c5 --steps 5 --warmup 3 --cpu-sample-s 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; tail -2 gpurun_out/bench_c5.err
-timeout 1200 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline --tensor-cores off > gpurun_out/bench_c5_ffma.json 2> gpurun_out/bench_c5_ffma.err
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain_b.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_l.log 2>&1
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_b2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"persist|rollout" -s 4 -c 1 -o gpurun_out/prof_c3_bench python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_f.log 2>&1
-python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain_c4.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c4.csv python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_l4.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:rollout_tc -s 3 -c 1 -o gpurun_out/prof_tc_c4 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_tc4.log 2>&1
-python bench.py --config c5 --instances 1024 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain_c5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:rollout_tc -s 3 -c 1 -o gpurun_out/prof_tc_c5 python bench.py --config c5 --instances 1024 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_tc5.log 2>&1
-tail -2 gpurun_out/ncu_f.log gpurun_out/ncu_tc4.log gpurun_out/ncu_tc5.log
+O=gpurun_out/r02; mkdir -p $O
+./tools/ffma_peak > $O/peaks.txt 2>&1
+timeout 1500 python -m pytest tests -q -m gpu --timeout 600 > $O/pytest_gpu_r02.log 2>&1; tail -2 $O/pytest_gpu_r02.log
+timeout 600 python bench.py > $O/bench_c3_r02.json 2> $O/bench_c3.err
+for c in c1 c2; do timeout 300 python bench.py --config $c > $O/bench_${c}_r02.json 2> $O/bench_$c.err; done
+timeout 900 python bench.py --config c4 --steps 10 --warmup 3 --cpu-sample-s 20 > $O/bench_c4_r02.json 2> $O/bench_c4.err
+timeout 1500 python bench.py --config c5 --steps 5 --warmup 3 --cpu-sample-s 20 > $O/bench_c5_r02.json 2> $O/bench_c5.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 2 > $O/bench_ref_c3_r02.json 2> $O/bench_ref.err
+timeout 600 python bench.py --impl reference --config c5 --steps 5 --warmup 1 > $O/bench_ref_c5_r02.json 2> $O/bench_ref5.err
+EMPC_PHASES=1 timeout 120 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 >/dev/null | grep -E "phases|persist" | tail -3 > $O/phases_c3_r02.txt
+for c in c1 c2 c3 c4; do
+  python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $O/launches_${c}_r02.csv python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:persist -s 2 -c 1 -o $O/prof_c3_persist_r02 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:small -s 2 -c 1 -o $O/prof_c1_small_r02 python bench.py --config c1 --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_c1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:select_radix -s 3 -c 1 -o $O/prof_c4_radix_r02 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_c4.log 2>&1
+for c in c1 c2 c3 c4 c5; do python -c "import json; d=json.load(open('$O/bench_${c}_r02.json')); print('$c', round(d['ms_per_step'],4), 'e2e med', round(d['e2e']['latency_ms_median'],4), 'mean', round(d['e2e']['latency_ms_mean'],4), 'frac', round(d['roofline']['frac'],3), d['roofline']['bound'], d['clocks'])"; done
