@@ -320,7 +320,13 @@ def _check_sched(spec, sched):
 
 
 def _has_state_bounds(spec) -> bool:
-    return getattr(spec, "x_min", None) is not None or getattr(spec, "x_max", None) is not None
+    """``MpcSpec.has_state_bounds`` (K/condense.py:83-87): a bound counts only
+    when it has a finite entry (all-infinite bounds keep the condensed scorer)."""
+    hb = getattr(spec, "has_state_bounds", None)
+    if isinstance(hb, bool):
+        return hb
+    lo, hi = getattr(spec, "x_min", None), getattr(spec, "x_max", None)
+    return bool((lo is not None and np.any(np.isfinite(lo))) or (hi is not None and np.any(np.isfinite(hi))))
 
 
 def _scorer_code(scorer: str, spec=None) -> int:

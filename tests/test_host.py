@@ -171,3 +171,26 @@ def test_breed_stream_statistics():
     assert parents.min() >= 0 and parents.max() < 64
     assert abs(take.mean() - 0.5) < 0.005 and abs(mut.mean() - 0.5) < 0.005
     assert abs(z.mean()) < 0.01 and abs(z.std() - 1.0) < 0.01
+
+
+def test_state_bounds_need_a_finite_entry():
+    """K/condense.py:83-87: all-infinite state bounds are no bounds (the
+    condensed scorer stays available)."""
+    import numpy as np
+
+    import paper_2001_04931_b200 as P
+    from paper_2001_04931_b200 import empc as E
+
+    model = P.DiscreteLinearModel(np.eye(2), np.ones((2, 1)), np.zeros(2), 0.01)
+    base = dict(Q=np.eye(2), R=np.eye(1), x_goal=np.zeros(2), u_goal=np.zeros(1), u_min=-np.ones(1),
+                u_max=np.ones(1))
+    inf = P.MpcSpec(model, 5, x_min=-np.inf * np.ones(2), x_max=np.inf * np.ones(2), **base)
+    fin = P.MpcSpec(model, 5, x_min=np.array([-np.inf, -3.0]), **base)
+    assert not E._has_state_bounds(inf) and E._scorer_code("condensed", inf) == 1
+    assert E._has_state_bounds(fin) and E._scorer_code("condensed", fin) == 0
+
+    class Dummy:  # duck-typed spec without the property
+        x_min = np.array([-np.inf, -np.inf])
+        x_max = None
+
+    assert not E._has_state_bounds(Dummy())
