@@ -151,9 +151,11 @@ class Engine final : public EngineBase {
     }
     CK(cudaMalloc(&elite_, sizeof(int) * (size_t)I_ * d_.K));
     qcap_ = std::max(1, d_.N - d_.K);  // every child may qualify: the list never overflows
-    CK(cudaMalloc(&qcount_, sizeof(int) * 2 * (size_t)I_));
-    CK(cudaMemset(qcount_, 0, sizeof(int) * 2 * (size_t)I_));
-    CK(cudaMalloc(&qlist_, sizeof(typename OrdOf<S>::T) * 2 * 2 * (size_t)I_ * qcap_));
+    // qualifier lists: two buffers for the per-generation launches, three
+    // for the one-barrier persistent solve
+    CK(cudaMalloc(&qcount_, sizeof(int) * 3 * (size_t)I_));
+    CK(cudaMemset(qcount_, 0, sizeof(int) * 3 * (size_t)I_));
+    CK(cudaMalloc(&qlist_, sizeof(typename OrdOf<S>::T) * 2 * 3 * (size_t)I_ * qcap_));
     out_stride_ = d_.m + d_.pm + 2;
     CK(cudaMalloc(&out_d_, sizeof(double) * (size_t)I_ * out_stride_));
     CK(cudaMallocHost(&out_h_, sizeof(double) * (size_t)I_ * out_stride_));
@@ -740,8 +742,12 @@ class Engine final : public EngineBase {
     // phases (they skip the recursion)
     if (v.ws) threads = std::max(threads, std::min(pv->maxt, ws_threads_) / 32 * 32);
     if (threads > pv->maxt) return false;
-    const size_t smem =
+    const size_t smem_plan_total =
         smem_plan<S>(v.NP, d_.m, d_.T, d_.p, tileP, tps_for(tileP), v.areg, v.dq, persist_select_smem()).total;
+    // one-barrier generations keep a K-entry rank -> row table after the plan
+    const bool one_sync = persist_radix() && one_sync_ok_;
+    const size_t elite_off = (smem_plan_total + 15) / 16 * 16;
+    const size_t smem = one_sync ? elite_off + sizeof(int) * (size_t)d_.K : smem_plan_total;
     if (smem > (size_t)kMaxSmem - 1024) return false;
     if (!persist_attr_set_) {
       for (auto& p : persist_)
@@ -775,6 +781,8 @@ class Engine final : public EngineBase {
     P.incremental = incremental_ ? 1 : 0;
     P.scratch = persist_select_smem();
     P.radix = persist_radix() ? 1 : 0;
+    P.one_sync = one_sync ? 1 : 0;
+    P.elite_off = elite_off;
     P.dbg_gen = -1;
     P.amin = sizeof(S) == 4 ? amin_d_ : nullptr;
     if (const char* e = std::getenv("EMPC_PHASES_GEN")) P.dbg_gen = std::atoi(e);
@@ -810,7 +818,8 @@ class Engine final : public EngineBase {
     ++rollout_launches_;
     if (timed) post();
     persist_desc_ = std::string("persistent grid=") + std::to_string(grid) + " threads=" + std::to_string(threads) +
-                    " smem=" + std::to_string(smem) + (pv->hk ? " halfK" : "") + (P.predraw ? " predraw" : "");
+                    " smem=" + std::to_string(smem) + (pv->hk ? " halfK" : "") + (P.predraw ? " predraw" : "") +
+                    (P.one_sync ? " onesync" : "");
     return true;
   }
 
@@ -1475,6 +1484,10 @@ class Engine final : public EngineBase {
   unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key
   int stagger_ = 0;       // WS recursion phase offset (cycles), EMPC_STAGGER
   bool predraw_ok_ = std::getenv("EMPC_NO_PREDRAW") == nullptr;
+  // one-barrier generations (redundant per-CTA selection): correct (the GPU
+  // tests pass in that mode) but measured slower at C3 (34.5 vs 31.3 us per
+  // generation), so opt-in
+  bool one_sync_ok_ = std::getenv("EMPC_ONE_SYNC") != nullptr;
   int ws_threads_ = 352;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)
   S *cw_ = nullptr, *G_ = nullptr;
   double *W64_ = nullptr, *G64_ = nullptr;  // FP64 W (T x p) and W'W for the condensed build

@@ -956,7 +956,8 @@ __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, i
                                                   int incremental, int* __restrict__ qcount_in,
                                                   const void* __restrict__ qlist_in, int* __restrict__ qcount_next,
                                                   int qcap, const S* __restrict__ pop_in, S* __restrict__ pop_out,
-                                                  S* __restrict__ cost_out, int pm) {
+                                                  S* __restrict__ cost_out, int pm, int* s_elite = nullptr,
+                                                  unsigned long long* fold_amin = nullptr) {
   static_assert(sizeof(S) == 4, "64-bit (ord32, row) keys: FP32 costs");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
@@ -1050,8 +1051,33 @@ __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, i
   for (int j = j0; j < j1; ++j)
     if (keys[j] <= thr) E[cnt++] = keys[j];
   __syncthreads();
-  // ---- rank this CTA's slice of the elites (K keys, unique)
   const int ne = min(K, total);
+  if (s_elite != nullptr) {
+    // redundant mode (one grid barrier per generation): every CTA ranks ALL
+    // K elites into its own shared rank -> row table (K^2 comparisons), then
+    // carries over only its slice of the elite rows for the next generation
+    for (int e = tid; e < ne; e += nthr) {
+      const unsigned long long ke = E[e];
+      int r = 0;
+      for (int j = 0; j < ne; ++j) r += E[j] < ke ? 1 : 0;
+      s_elite[r] = (int)(uint32_t)ke;
+    }
+    __syncthreads();
+    const int per = (ne + gridDim.x - 1) / gridDim.x;
+    const int r0 = blockIdx.x * per, r1 = min(ne, r0 + per);
+    for (int r = r0 + warp; r < r1; r += nwarps) {
+      const int re = s_elite[r];
+      const S* from = pop_in + ((size_t)inst * N + re) * pm;
+      S* to = pop_out + ((size_t)inst * N + r) * pm;
+      for (int g = lane; g < pm; g += 32) to[g] = from[g];
+      if (lane == 0) {
+        cost_out[(size_t)inst * N + r] = c[re];
+        if (fold_amin != nullptr) atomicMin(fold_amin, amin_key(c[re], r));  // the final population's elites
+      }
+    }
+    return;
+  }
+  // ---- rank this CTA's slice of the elites (K keys, unique)
   const int per = (ne + gridDim.x - 1) / gridDim.x;
   const int e0 = blockIdx.x * per, e1 = min(ne, e0 + per);
   for (int e = e0 + warp; e < e1; e += nwarps) {
@@ -1327,13 +1353,15 @@ struct PersistArgs {
   S* pop[2];
   S* cost[2];
   int* qcount;        // [2] double-buffered qualifier counts
-  void* qlist;        // [2][qcap] (key, row) pairs
+  void* qlist;        // [3][qcap] (key, row) pairs (two used unless one_sync)
   int* elite;         // elite_idx (written by the selection)
   double* out;
   int predraw;        // WS variant with helper warps: next-generation draws during the recursion
   int radix;          // selection by radix select (FP32)
   int dbg_gen;        // EMPC_PHASES: evolve whose phases are recorded (-1: every one, the last wins)
   unsigned long long* amin;  // distributed argmin key (FP32), NULL: CTA 0 scans the population
+  int one_sync;       // one grid barrier per generation (redundant per-CTA selection, FP32)
+  size_t elite_off;   // shared-memory offset of the per-CTA rank -> row table (one_sync)
   // injected draws of the evolves (parity mode; NULL: in-kernel Philox):
   // evolve g reads parents + g (N-K) 2, masks / noise + g (N-K) p m
   const int* inj_parents;
@@ -1341,6 +1369,11 @@ struct PersistArgs {
   const uint8_t* inj_mut;
   const double* inj_noise;
 };
+
+__device__ __forceinline__ unsigned char* smem_raw_persist() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return smem_raw;
+}
 
 template <typename S, int NP, int RR, int CC, bool AREG, bool DQ, int KS, bool WS, int MAXT, bool HK = false>
 __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P) {
@@ -1368,6 +1401,14 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(a, true, P.scratch);
   if (gt) gt[1] = gtimer();
   int cur = 0;
+  // one-barrier generations (FP32): every CTA computes the whole selection
+  // itself (radix select + ranking of the K elites into a shared table), so
+  // breeding needs no second grid barrier.  Qualifier lists rotate over
+  // three buffers: evolve g appends to B[g % 3], its selection reads
+  // B[(g-1) % 3] and clears B[(g+1) % 3] (last read by evolve g-1's
+  // selection, next appended after the next barrier); B[0] is cleared here.
+  int* s_elite = (sizeof(S) == 4 && P.one_sync) ? reinterpret_cast<int*>(smem_raw_persist() + P.elite_off) : nullptr;
+  if (s_elite != nullptr && blockIdx.x == 0 && threadIdx.x == 0) P.qcount[0] = 0;
   for (int g = 0; g < P.evolves; ++g) {
     if (gt && g > 0 && g + 1 < 30) gt[g + 1] = gtimer();
     EMPC_MARK(13)
@@ -1375,7 +1416,13 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     EMPC_MARK(14)
     const int inc = (g > 0 && P.incremental) ? 1 : 0;
     if constexpr (sizeof(S) == 4) {
-      if (P.radix && !inc) {
+      if (s_elite != nullptr) {
+        select_radix_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g + 2) % 3) : nullptr,
+                             (const char*)P.qlist + ((g + 2) % 3) * qstride, P.qcount + ((g + 1) % 3), a.qcap,
+                             P.pop[cur], P.pop[cur ^ 1], P.cost[cur ^ 1], pm, s_elite,
+                             (dist_amin && g + 1 == P.evolves) ? P.amin : nullptr);
+        __syncthreads();  // s_elite complete; the scratch is the rollout's again
+      } else if (P.radix && !inc) {
         // the first selection ranks all N candidates (35 us by counting at
         // C3): radix select of the K-th key + ranking of the K elites only.
         // Later (incremental) sets are small enough for rank-by-counting,
@@ -1394,7 +1441,7 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
                      P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
     }
     EMPC_MARK(15)
-    grid.sync();
+    if (s_elite == nullptr) grid.sync();
     RolloutArgs<S> b = a;
     b.mode = P.inj_parents != nullptr ? kBreedInject : kBreedPhilox;
     if (P.dbg_gen >= 0) b.dbg = g == P.dbg_gen ? a.dbg : nullptr;  // phase marks of one chosen evolve
@@ -1411,7 +1458,8 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     b.tile = P.tile_evolve;
     b.evolve = g;
     b.copy_elites = 0;
-    b.parents_from_out = 1;
+    b.parents_from_out = s_elite == nullptr ? 1 : 0;  // one-barrier mode: parents via the shared table, from pop_in
+    if (s_elite != nullptr) b.elite_idx = s_elite;
     // the helpers of a CTA without init candidates never ran (it returned
     // early), so its first evolve draws inline
     b.draws_ready = P.predraw && (g > 0 || (int)blockIdx.x * a.tile < a.nc);
@@ -1421,13 +1469,14 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     b.cost_in = P.cost[cur];
     b.pop_out = P.pop[cur ^ 1];
     b.cost_out = P.cost[cur ^ 1];
-    b.qcount = P.incremental ? P.qcount + (g & 1) : nullptr;
-    b.qlist = (char*)P.qlist + (g & 1) * qstride;
+    const int qb = s_elite != nullptr ? g % 3 : (g & 1);
+    b.qcount = P.incremental ? P.qcount + qb : nullptr;
+    b.qlist = (char*)P.qlist + qb * qstride;
     rollout_body<S, NP, RR, CC, AREG, DQ, KS, WS, HK>(b, false, P.scratch);
     cur ^= 1;
   }
   if (gt && P.evolves > 0 && P.evolves + 1 < 30) gt[P.evolves + 1] = gtimer();
-  if (dist_amin && P.evolves > 0) {
+  if (dist_amin && P.evolves > 0 && s_elite == nullptr) {
     // the elite rows [0, K) of the final population, a slice per CTA
     const int per = (K + gridDim.x - 1) / gridDim.x;
     for (int r = blockIdx.x * per + threadIdx.x; r < min(K, (int)(blockIdx.x + 1) * per); r += blockDim.x)
