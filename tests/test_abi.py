@@ -44,7 +44,7 @@ def test_rollout_kernels_use_fp32_fma():
     C3 variant's SASS is dominated by FFMA and carries no legacy HMMA path."""
     if not os.path.exists(nat.LIB_PATH):
         pytest.skip("library not built")
-    listing = subprocess.run(["cuobjdump", "-sass", nat.LIB_PATH], capture_output=True, text=True).stdout
+    listing = _function_names()
     names = re.findall(r"Function : (_ZN4empc14rollout_kernelIfLi48ELi2ELi4ELb1ELb0ELi2E\S*)", listing)
     assert names, "default C3 rollout variant (NP48 RR2 CC4 areg ks2) not compiled"
     sass = subprocess.run(["cuobjdump", "-sass", "-fun", names[0], nat.LIB_PATH], capture_output=True,
@@ -70,3 +70,30 @@ def _load_missing(tmp_path):
         nat.load(str(tmp_path / "nope.so"))
     finally:
         nat._lib = saved
+
+
+def test_benched_persistent_kernel_is_ffma_and_uses_no_local_memory():
+    """The benched C3 kernel (persist_kernel, warp-synchronous NP48 RR3 CC4
+    KS2, half-K, 384-thread bound): FFMA recursion, no HMMA, no register
+    spills to local memory (which would put the state recursion on L1)."""
+    if not os.path.exists(nat.LIB_PATH):
+        pytest.skip("library not built")
+    listing = _function_names()
+    names = re.findall(r"Function : (_ZN4empc14persist_kernelIfLi48ELi3ELi4ELb1ELb0ELi2ELb1ELi384ELb1E\S*)", listing)
+    assert names, "benched persistent variant not compiled"
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", names[0], nat.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert sass.count("FFMA") >= 144  # 12 half-K columns x 3 rows x 4 candidates per step
+    assert "HMMA" not in sass
+    assert "STL" not in sass and "LDL" not in sass
+
+
+_NAMES = []
+
+
+def _function_names() -> str:
+    """'Function : <mangled>' lines of the library's SASS (listed once)."""
+    if not _NAMES:
+        out = subprocess.run(["cuobjdump", "-sass", nat.LIB_PATH], capture_output=True, text=True).stdout
+        _NAMES.append("\n".join(line for line in out.splitlines() if "Function :" in line))
+    return _NAMES[0]
