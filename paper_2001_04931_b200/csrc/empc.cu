@@ -130,7 +130,7 @@ class Engine final : public EngineBase {
     SL_.ug = s; s += m;
     SL_.umin = s; s += m;
     SL_.umax = s; s += m;
-    SL_.stride = s;
+    SL_.stride = s + (s & 1);  // even: every instance's block starts 16-byte aligned (async staging copies)
     SL_.x0 = 0;
     SL_.sig = n;
     SL_.sstride = n + m;

@@ -428,6 +428,22 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   // ---- phase 0: problem -> smem (coalesced, all loads in flight together);
   // a persistent CTA stages even when its first tile is empty (later ones are not)
   if (stage && (cnt > 0 || persist_scratch)) {
+    // [Ad | Bd | wd] (contiguous FP64 in the staging block, 16-byte aligned:
+    // the host pads the per-instance stride to an even number of doubles)
+    // goes to the scratch head with asynchronous 16-byte copies, all in
+    // flight at once, while the small arrays below load; converted from
+    // shared memory afterwards.  Falls back to direct loads when the scratch
+    // head (before XC, which may alias Bs) is too small.
+    const int nraw = n * n + n * m + n;
+    const bool raw_ok = (size_t)nraw * 8 + 16 <= sp.us + sp.but;
+    const double* raw = reinterpret_cast<const double*>(smem_raw);
+    if (raw_ok) {
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+      for (int q = tid; q < (nraw + 1) / 2; q += nthr)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + 16u * (uint32_t)q),
+                     "l"(P + SL.ad + 2 * q));
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
     for (int k = tid; k < T; k += nthr) {
       sI1[k] = a.idx1[k];
       sI2[k] = a.idx2[k];
@@ -435,16 +451,22 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
       sC[k] = a.cw[k];
     }
     for (int e = tid; e < p * p; e += nthr) sG[e] = a.G[e];
+    if (raw_ok) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+    }
+    const double* Ad = raw_ok ? raw : P + SL.ad;
+    const double* Bd = raw_ok ? raw + n * n : P + SL.bd;
 #pragma unroll 8
     for (int e = tid; e < NP * NP; e += nthr) {
       const int i = e / NP, j = e - (e / NP) * NP;
-      As[i * NPS + j] = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
+      As[i * NPS + j] = (i < n && j < n) ? (S)(Ad[i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
       if constexpr (DQ) Qs[i * NPS + j] = (i < n && j < n) ? (S)P[SL.q + i * n + j] : S(0);
     }
 #pragma unroll 8
     for (int e = tid; e < NP * m; e += nthr) {
       const int i = e / m, l = e - (e / m) * m;
-      Bs[i * (m + 1) + l] = i < n ? (S)P[SL.bd + i * m + l] : S(0);
+      Bs[i * (m + 1) + l] = i < n ? (S)Bd[i * m + l] : S(0);
     }
     // the recursion runs in error coordinates e = x - x_goal:
     //   e_{k+1} = e_k + Delta e_k + (drive_k + Delta x_goal)
