@@ -635,7 +635,10 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
       }
     }
   }
-  __syncthreads();  // Bs (in XC) consumed; BUT / cU visible
+  // Bs aliases XC in the per-generation kernels: consumed before the fill
+  // (the persistent solve keeps Bs apart, and the barrier after the fill
+  // also publishes BUT)
+  if (!persist_scratch) __syncthreads();
   // x_0 = x0 for every candidate (K/empc.py:109)
   for (int e = tid; e < tileP * NPS; e += nthr) {
     const int i = e % NPS;
