@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--num-sims", type=int, default=None,
                     help="override the population size N (e.g. one rank's share of a sharded C4 population)")
     ap.add_argument("--variant", type=int, default=-1, help="force a rollout kernel variant")
+    ap.add_argument("--sharded", action="store_true",
+                    help="C4: run the population-sharded solve (shard.py) also at one GPU -- the N = 1 point of the "
+                         "population-sharding scaling curve")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tensor-cores", default="auto", choices=["auto", "on", "off"],
@@ -284,6 +287,8 @@ def run_population_sharded(args, rank, world):
     gathered = torch.empty(world * K * eb, dtype=torch.uint8, device="cuda")
 
     def all_gather(local):
+        if world == 1:
+            return local
         dist.all_gather_into_tensor(gathered, local)
         return gathered
 
@@ -294,7 +299,8 @@ def run_population_sharded(args, rank, world):
     stream = torch.cuda.ExternalStream(shard.stream_ptr)
     sampler = ClockSampler(0)
     times = []
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -303,10 +309,12 @@ def run_population_sharded(args, rank, world):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     clocks = sampler.stop()
     t = torch.tensor([sum(times)], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     units = w.cand_steps_per_solve * args.steps
     value = units / (total_ms * 1e-3)
@@ -324,7 +332,8 @@ def run_population_sharded(args, rank, world):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_baseline(args, w, specs, x0s):
@@ -371,7 +380,7 @@ def run_ours(args):
     from paper_2001_04931_b200 import _native as nat
     from paper_2001_04931_b200 import empc as E
 
-    if world > 1 and args.config == "c4":
+    if args.config == "c4" and (world > 1 or args.sharded):
         return run_population_sharded(args, rank, world)
     w_total, w, specs, x0s, scaling = workload(args, rank, world)
     sched = w.schedule()
@@ -467,6 +476,27 @@ def run_ours(args):
                  "latency_ms_q1": float(np.percentile(e2e_ms, 25)), "latency_ms_q3": float(np.percentile(e2e_ms, 75)),
                  "latency_ms_mean": float(e2e_ms.mean()), "latency_ms_max": float(e2e_ms.max()),
                  "slowest_call": int(np.argmax(e2e_ms))}
+    # warm start (cold and warm): solve_empc(prev=population)
+    # with the population resident on the GPU, as a closed loop calls it
+    # (K/closedloop.py:109): re-score at x0 + G generations, same model
+    if w.instances == 1:
+        prev = P.solve_empc(specs[0], sched, st, x0s[0]).population
+        for _ in range(5):
+            prev = P.solve_empc(specs[0], sched, st, x0s[0], prev=prev).population
+        gc.collect()
+        gc.freeze()
+        warm = []
+        for _ in range(n_e2e):
+            t0 = time.perf_counter()
+            prev = P.solve_empc(specs[0], sched, st, x0s[0], prev=prev).population
+            warm.append(time.perf_counter() - t0)
+        gc.unfreeze()
+        wm = np.asarray(warm) * 1e3
+        e2e_stats["warm"] = {"calls": n_e2e, "latency_ms_median": float(np.median(wm)),
+                             "latency_ms_q1": float(np.percentile(wm, 25)),
+                             "latency_ms_q3": float(np.percentile(wm, 75)), "latency_ms_mean": float(wm.mean()),
+                             "scored_per_solve": w.N + w.G * (w.N - w.K),
+                             "note": "solve_empc(prev=population): re-score + G generations, population on the GPU"}
 
     # --- roofline of the dominant kernel (rollout: K2+K3 with the K5 prologue)
     condensed = args.scorer == "condensed"

@@ -1253,6 +1253,7 @@ class Engine final : public EngineBase {
     if (!sh_attr_set_) {
       CK(cudaFuncSetAttribute(shard_export_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
       CK(cudaFuncSetAttribute(shard_import_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
+      CK(cudaFuncSetAttribute(shard_export_radix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024));
       sh_attr_set_ = true;
     }
     pdl_next_ = false;
@@ -1272,6 +1273,16 @@ class Engine final : public EngineBase {
     const int nl = sh_init_phase_ ? sh_init_ : sh_children_;
     const long long gbase = sh_init_phase_ ? sh_init_base_ : (long long)d_.K + sh_child_base_;
     const int M = (incl ? d_.K : 0) + nl;
+    if constexpr (sizeof(S) == 4) {
+      const size_t rsm = shard_export_radix_smem(M, d_.K);
+      if (rsm <= (size_t)kMaxSmem - 1024 && M >= 2048) {  // large shards: radix select
+        shard_export_radix_kernel<<<rank_grid(d_.K), 1024, rsm, stream_>>>(
+            (const float*)pop_[sh_cur_], (const float*)cost_[sh_cur_], d_.K, d_.pm, incl, nl, gbase,
+            (unsigned char*)dev_out);
+        CK(cudaGetLastError());
+        return;
+      }
+    }
     const size_t smem = (size_t)M * (sizeof(typename OrdOf<S>::T) + 2 * sizeof(int));
     if (smem > (size_t)kMaxSmem - 1024) throw InvalidArg{"shard too large for the export kernel"};
     shard_export_kernel<S><<<rank_grid(M), 256, smem, stream_>>>(pop_[sh_cur_], cost_[sh_cur_], d_.K, d_.pm, incl, nl,

@@ -976,41 +976,15 @@ __device__ __forceinline__ void block_exclusive_scan(int& v, int* warp_tot, int&
   __syncthreads();
 }
 
-template <typename S>
-__device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
-                                                  int incremental, int* __restrict__ qcount_in,
-                                                  const void* __restrict__ qlist_in, int* __restrict__ qcount_next,
-                                                  int qcap, const S* __restrict__ pop_in, S* __restrict__ pop_out,
-                                                  S* __restrict__ cost_out, int pm, int* s_elite = nullptr,
-                                                  unsigned long long* fold_amin = nullptr) {
-  static_assert(sizeof(S) == 4, "64-bit (ord32, row) keys: FP32 costs");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
-  const int inst = blockIdx.y;
-  const S* c = costs + (size_t)inst * N;
+// The K smallest of M unique 64-bit keys in shared memory: 8-bit radix
+// select of the K-th key (warp-aggregated histograms, early exit when the
+// bucket is taken whole), then a deterministic compaction of the keys <= it
+// into E in key-position order (block scan).  total = number compacted
+// (min(K, M)).  All threads of the block call it.
+__device__ __forceinline__ void radix_topk_compact(const unsigned long long* keys, int M, int K,
+                                                   unsigned long long* E, int* hist, int* aux, int& total) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
-  pdl_wait();
-  int L = 0;
-  bool full = !incremental || K >= N || qcount_in == nullptr;
-  if (!full) {
-    L = qcount_in[inst];
-    full = L > qcap || K + L > N;
-  }
-  const int M = full ? N : K + L;
-  unsigned long long* E = keys + N;                    // [K] elite keys in key-position order
-  int* hist = reinterpret_cast<int*>(E + K);           // [256]
-  int* aux = hist + 256;                               // [64]: warp totals, bucket / remainder broadcast
-  __syncthreads();  // all reads of the count precede its reset below
-  if (blockIdx.x == 0 && tid == 0 && qcount_next != nullptr) qcount_next[inst] = 0;
-  pdl_trigger();
-  const uint32_t* ql = full ? nullptr : reinterpret_cast<const uint32_t*>(qlist_in) + (size_t)inst * qcap * 2;
-  for (int j = tid; j < M; j += nthr) {
-    unsigned long long k;
-    if (j < K || full) k = ((unsigned long long)ord32((float)c[j]) << 32) | (unsigned)j;
-    else k = ((unsigned long long)ql[2 * (j - K)] << 32) | ql[2 * (j - K) + 1];
-    keys[j] = k;
-  }
   // ---- radix select of the K-th smallest key: prefix / mask of the bucket
   unsigned long long prefix = 0ull, mask = 0ull;
   int krem = K;
@@ -1071,11 +1045,49 @@ __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, i
   const int j0 = min(M, tid * chunk), j1 = min(M, j0 + chunk);
   int cnt = 0;
   for (int j = j0; j < j1; ++j) cnt += keys[j] <= thr ? 1 : 0;
-  int total;
   block_exclusive_scan(cnt, aux, total);
   for (int j = j0; j < j1; ++j)
     if (keys[j] <= thr) E[cnt++] = keys[j];
   __syncthreads();
+}
+
+template <typename S>
+__device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
+                                                  int incremental, int* __restrict__ qcount_in,
+                                                  const void* __restrict__ qlist_in, int* __restrict__ qcount_next,
+                                                  int qcap, const S* __restrict__ pop_in, S* __restrict__ pop_out,
+                                                  S* __restrict__ cost_out, int pm, int* s_elite = nullptr,
+                                                  unsigned long long* fold_amin = nullptr) {
+  static_assert(sizeof(S) == 4, "64-bit (ord32, row) keys: FP32 costs");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
+  const int inst = blockIdx.y;
+  const S* c = costs + (size_t)inst * N;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  pdl_wait();
+  int L = 0;
+  bool full = !incremental || K >= N || qcount_in == nullptr;
+  if (!full) {
+    L = qcount_in[inst];
+    full = L > qcap || K + L > N;
+  }
+  const int M = full ? N : K + L;
+  unsigned long long* E = keys + N;                    // [K] elite keys in key-position order
+  int* hist = reinterpret_cast<int*>(E + K);           // [256]
+  int* aux = hist + 256;                               // [64]: warp totals, bucket / remainder broadcast
+  __syncthreads();  // all reads of the count precede its reset below
+  if (blockIdx.x == 0 && tid == 0 && qcount_next != nullptr) qcount_next[inst] = 0;
+  pdl_trigger();
+  const uint32_t* ql = full ? nullptr : reinterpret_cast<const uint32_t*>(qlist_in) + (size_t)inst * qcap * 2;
+  for (int j = tid; j < M; j += nthr) {
+    unsigned long long k;
+    if (j < K || full) k = ((unsigned long long)ord32((float)c[j]) << 32) | (unsigned)j;
+    else k = ((unsigned long long)ql[2 * (j - K)] << 32) | ql[2 * (j - K) + 1];
+    keys[j] = k;
+  }
+  int total;
+  radix_topk_compact(keys, M, K, E, hist, aux, total);
   const int ne = min(K, total);
   if (s_elite != nullptr) {
     // redundant mode (one grid barrier per generation): every CTA ranks ALL
@@ -1209,6 +1221,72 @@ __global__ void __launch_bounds__(256) shard_export_kernel(const S* __restrict__
     }
   }
 }
+
+// FP32 export by radix select (the local set is K elites + ~(N-K)/W
+// children: O(M^2) ranking dominated the one-rank C4 shard at 16k rows).
+// Same entries, same order as shard_export_kernel.  One CTA per slice of
+// the K output ranks; every CTA finds the K-th key itself.
+__host__ __device__ inline size_t shard_export_radix_smem(int M, int K) {
+  return (size_t)M * 8 + (size_t)M * 4 + (size_t)K * 8 + 256 * 4 + 64 * 4 + 64;
+}
+
+#ifdef EMPC_HOST_TU
+__global__ void __launch_bounds__(1024) shard_export_radix_kernel(const float* __restrict__ pop,
+                                                                  const float* __restrict__ costs, int K, int pm,
+                                                                  int incl_elites, int n_local, long long gbase,
+                                                                  unsigned char* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int E0 = incl_elites ? K : 0;
+  const int M = E0 + n_local;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);  // (ord, global row)
+  int* lr = reinterpret_cast<int*>(keys + M);                                     // local rows
+  unsigned long long* E = reinterpret_cast<unsigned long long*>(lr + M + (M & 1));
+  int* hist = reinterpret_cast<int*>(E + K);
+  int* aux = hist + 256;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const size_t eb = shard_entry_bytes<float>(pm);
+  pdl_wait();
+  for (int j = tid; j < M; j += nthr) {
+    const int row = j < E0 ? j : K + (j - E0);
+    const unsigned grow = j < E0 ? (unsigned)j : (unsigned)(gbase + (j - E0));
+    lr[j] = row;
+    keys[j] = ((unsigned long long)ord32(costs[row]) << 32) | grow;
+  }
+  if (blockIdx.x == 0)  // sentinels when this rank holds fewer than K candidates
+    for (int r = M + tid; r < K; r += nthr) {
+      unsigned char* e = out + (size_t)r * eb;
+      *reinterpret_cast<unsigned long long*>(e) = ~0ull;
+      *reinterpret_cast<unsigned*>(e + 8) = 0xFFFFFFFFu - (unsigned)r;
+      *reinterpret_cast<unsigned*>(e + 12) = 0u;
+    }
+  int total;
+  radix_topk_compact(keys, M, K, E, hist, aux, total);
+  const int ne = min(K, total);
+  const int per = (ne + gridDim.x - 1) / gridDim.x;
+  const int e0 = blockIdx.x * per, e1 = min(ne, e0 + per);
+  for (int e = e0 + warp; e < e1; e += nwarps) {
+    const unsigned long long ke = E[e];
+    int r = 0;
+    for (int j = lane; j < ne; j += 32) r += E[j] < ke ? 1 : 0;
+    r = __reduce_add_sync(0xFFFFFFFFu, r);
+    // local row of this key: the global row identifies it uniquely
+    const unsigned grow = (unsigned)ke;
+    const int row = grow < (unsigned)E0 ? (int)grow : K + (int)((long long)grow - gbase);
+    unsigned char* ent = out + (size_t)r * eb;
+    const float* g = pop + (size_t)row * pm;
+    if (lane == 0) {
+      // the entry key is the 32-bit orderable cost, as shard_export_kernel writes it
+      *reinterpret_cast<unsigned long long*>(ent) = (unsigned long long)(uint32_t)(ke >> 32);
+      *reinterpret_cast<unsigned*>(ent + 8) = grow;
+      *reinterpret_cast<unsigned*>(ent + 12) = 1u;
+      *reinterpret_cast<float*>(ent + 16) = costs[row];
+    }
+    float* dst = reinterpret_cast<float*>(ent + 24);
+    for (int q = lane; q < pm; q += 32) dst[q] = g[q];
+  }
+  (void)lr;
+}
+#endif  // EMPC_HOST_TU
 
 template <typename S>
 __global__ void __launch_bounds__(256) shard_import_kernel(const unsigned char* __restrict__ all, int M, int K, int pm,
