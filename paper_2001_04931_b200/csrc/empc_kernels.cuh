@@ -365,6 +365,45 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
 // (1) wait for the producer, elite carry-over and breeding; (2) B at the
 // knots and the knot-space input cost; (3) the horizon recursion.
 
+// Input cost of a tile's candidates as the knot quadratic
+// z'(W'W (x) R) z, z = U - u_goal (K/empc.py:100-101), for small state sizes
+// (NP <= 16: few row groups, so the per-row-group channel split below leaves
+// most threads idle): eight lanes per candidate take the channels
+// l = lane8 (mod 8) and fold with a fixed shuffle tree; nt is a multiple of 32.
+template <typename S>
+__device__ __forceinline__ void input_costs(S* __restrict__ icost, const S* __restrict__ UsT, int tPS, int cnt, int m,
+                                            int p, const S* sG, const S* cug, const S* crd, bool r_diag,
+                                            const double* Rg, int nt) {
+  const int t = threadIdx.x;
+  const int g8 = (t & 31) >> 3, l8 = t & 7, w = t >> 5, nw = nt >> 5;
+  for (int cb = 4 * w; cb < cnt; cb += 4 * nw) {  // warp-uniform trip count
+    const int c = cb + g8;
+    S val = S(0);
+    if (c < cnt) {
+      for (int l = l8; l < m; l += 8) {
+        for (int q = 0; q < p; ++q) {
+          S gz = S(0);
+          for (int b = 0; b < p; ++b) {
+            S rz;
+            if (r_diag) {
+              rz = crd[l] * (UsT[(b * m + l) * tPS + c] - cug[l]);
+            } else {
+              rz = S(0);
+              for (int l2 = 0; l2 < m; ++l2) rz = fma((S)Rg[l * m + l2], UsT[(b * m + l2) * tPS + c] - cug[l2], rz);
+            }
+            gz = fma(sG[q * p + b], rz, gz);
+          }
+          val = fma(UsT[(q * m + l) * tPS + c] - cug[l], gz, val);
+        }
+      }
+    }
+    val += __shfl_xor_sync(0xFFFFFFFFu, val, 4);
+    val += __shfl_xor_sync(0xFFFFFFFFu, val, 2);
+    val += __shfl_xor_sync(0xFFFFFFFFu, val, 1);
+    if (l8 == 0 && c < cnt) icost[c] = val;
+  }
+}
+
 // HK: the left half of Delta's columns is exactly zero (the position columns
 // of a linearized mechanism without gravity): the matvec runs over
 // the right half only, split over the lane pair as usual (exact: the skipped
@@ -592,7 +631,11 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   S cst[CH];
 #pragma unroll
   for (int q = 0; q < CH; ++q) cst[q] = S(0);
-  if (active) {
+  constexpr bool kCoopIcost = NP <= 16;
+  S* icost = reinterpret_cast<S*>(reinterpret_cast<unsigned char*>(src) - sp.cu);  // the plan's per-candidate slot
+  if constexpr (kCoopIcost)
+    input_costs<S>(icost, UsT, tPS, cnt, m, p, sG, cug, crd, a.r_diag != 0, P + SL.r, (nthr + 31) / 32 * 32);
+  if (active && !kCoopIcost) {
     for (int l = rg; l < m; l += NRG) {
       const S ugl = cug[l];
 #pragma unroll
@@ -815,6 +858,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   if (qual) tau = ord_key(a.cost_in[pop_base + a.elite_idx[(size_t)inst * d.K + d.K - 1]]);
   for (int c = tid; c < cnt; c += nthr) {
     S s = S(0);
+    if constexpr (kCoopIcost) s = icost[c];
     for (int g = 0; g < NRG; ++g) s += red[g * tPS + c];
     const S cost = c0s + s;
     const int row = a.row0 + tile0 + c;
