@@ -859,6 +859,10 @@ class Engine final : public EngineBase {
     }
     // (draws and selection use every thread; scoring one thread per candidate)
     const int threads = std::min(512, std::max(small_threads_, (d_.N + 31) / 32 * 32));
+    if (phases_) {
+      A.dbg = dbg_;
+      small_dbg_ = true;
+    }
     if (timed) pre();
     launch_ex(kern, dim3(I_), dim3(threads), smem, false, A);
     ++launches_;
@@ -1176,6 +1180,12 @@ class Engine final : public EngineBase {
       }
       *rollout_ms = (float)(sum / ((double)reps2 * std::max(nr, 1)));
     }
+    if (phases_ && small_dbg_) {  // resident small solve: cycles per phase, summed over generations
+      unsigned long long t[7];
+      CK(cudaMemcpy(t, dbg_, sizeof t, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "small solve phases (cycles, all generations): keys=%llu rank=%llu draws=%llu breed=%llu score=%llu"
+                   " (thread 0: input cost %llu, drive + recursion %llu)\n", t[0], t[1], t[2], t[3], t[4], t[5], t[6]);
+    }
     if (phases_ && dbg_ctas_ > 0) {
       // phase marks of the last rollout launch: mean over CTAs, relative to each CTA's start
       std::vector<unsigned long long> t((size_t)dbg_ctas_ * 16);
@@ -1472,7 +1482,7 @@ class Engine final : public EngineBase {
   int persist_tile_ = 0;   // minimum candidates per persistent CTA (0: one wave over the SMs)
   int small_mode_ = -1;    // resident single-CTA solve: -1 auto, 0 off, 1 whenever it fits
   int small_threads_ = 512;
-  bool small_attr_set_ = false;
+  bool small_attr_set_ = false, small_dbg_ = false;
   std::string small_desc_;
   bool persist_attr_set_ = false;
   std::vector<PersistVariant<S>> persist_;

@@ -46,7 +46,8 @@ __host__ __device__ inline size_t small_smem_bytes(int n, int m, int T, int p, i
 // drive = W (x) (U Bd') + w', recursion over the knot segments, diag-Q cost.
 template <typename S, int NPV>
 __device__ __forceinline__ S small_score(const S* __restrict__ U, const SmallShared<S>& sh, int m, int p, int T,
-                                      int r_diag) {
+                                      int r_diag, long long* prof = nullptr) {
+  long long t0 = prof ? clock64() : 0;
   // the model in registers (a reference parameter would force it to local memory)
   S Dr[NPV][NPV];
 #pragma unroll
@@ -55,12 +56,14 @@ __device__ __forceinline__ S small_score(const S* __restrict__ U, const SmallSha
     for (int j = 0; j < NPV; ++j) Dr[i][j] = sh.D[i * NPV + j];
   S st = sh.G[p * p];
   // input cost z'(W'W (x) R) z, z = U - u_goal (K/empc.py:100-101)
-#pragma unroll 2
+  // (runtime-bounded loops stay rolled: unrolled remainders blew the kernel
+  // up to ~18k instructions and the scorer ran out of the instruction cache)
+#pragma unroll 1
   for (int l = 0; l < m; ++l) {
-#pragma unroll 2
+#pragma unroll 1
     for (int t = 0; t < p; ++t) {
       S gz = S(0);
-#pragma unroll 4
+#pragma unroll 1
       for (int b = 0; b < p; ++b) {
         S rz;
         if (r_diag) {
@@ -80,6 +83,7 @@ __device__ __forceinline__ S small_score(const S* __restrict__ U, const SmallSha
     e[i] = sh.E0[i];
     srow[i] = S(0);
   }
+  if (prof) { const long long t1 = clock64(); prof[0] += t1 - t0; t0 = t1; }
 #pragma unroll 1
   for (int k0 = 0; k0 < T;) {
     const int k1 = sh.Seg[k0], i1 = sh.I1[k0], i2 = sh.I2[k0];
@@ -87,7 +91,7 @@ __device__ __forceinline__ S small_score(const S* __restrict__ U, const SmallSha
 #pragma unroll
     for (int i = 0; i < NPV; ++i) {
       S u1 = sh.W[i], u2 = sh.W[i];
-#pragma unroll 4
+#pragma unroll 1
       for (int l = 0; l < m; ++l) {
         u1 = fma(sh.B[i * m + l], U[i1 * m + l], u1);
         u2 = fma(sh.B[i * m + l], U[i2 * m + l], u2);
@@ -116,6 +120,7 @@ __device__ __forceinline__ S small_score(const S* __restrict__ U, const SmallSha
   }
 #pragma unroll
   for (int i = 0; i < NPV; ++i) st = fma(sh.Q[i], srow[i], st);
+  if (prof) prof[1] += clock64() - t0;
   return st;
 }
 
@@ -148,12 +153,13 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   int* sSeg = sI2 + T;
   S* sC = reinterpret_cast<S*>(sSeg + T); ptr += al((size_t)T * (3 * sizeof(int) + sizeof(S)));
   S* sG = reinterpret_cast<S*>(ptr); ptr += al((size_t)(p * p + 2) * sizeof(S));
-  S* pop[2];
-  pop[0] = reinterpret_cast<S*>(ptr);
-  pop[1] = pop[0] + (size_t)N * pm; ptr += al((size_t)2 * N * pm * sizeof(S));
-  S* cost[2];
-  cost[0] = reinterpret_cast<S*>(ptr);
-  cost[1] = cost[0] + N; ptr += al((size_t)2 * N * sizeof(S));
+  // two populations / cost vectors as plain pointers (an array of pointers
+  // indexed by the generation parity would live in local memory and turn
+  // every shared access into a generic one)
+  S* const popA = reinterpret_cast<S*>(ptr);
+  S* const popB = popA + (size_t)N * pm; ptr += al((size_t)2 * N * pm * sizeof(S));
+  S* const costA = reinterpret_cast<S*>(ptr);
+  S* const costB = costA + N; ptr += al((size_t)2 * N * sizeof(S));
   OT* keys = reinterpret_cast<OT*>(ptr); ptr += al((size_t)(N > 64 ? N : 64) * 8);
   int* src = reinterpret_cast<int*>(ptr); ptr += al((size_t)nc * 2 * sizeof(int));
   uint8_t* tbits = reinterpret_cast<uint8_t*>(ptr); ptr += al((size_t)nc * pm);
@@ -201,7 +207,9 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   }
   __syncthreads();
   const SmallShared<S> sh{sD, sW, sQ, sE0, sB, sUg, sRd, sR, sG, sC, sI1, sI2, sSeg};
-  auto score = [&](const S* U) -> S { return small_score<S, NPV>(U, sh, m, p, T, A.r_diag); };
+  long long sprof[2] = {0, 0};
+  const bool prof_on = A.dbg != nullptr && inst == 0 && tid == 0;
+  auto score = [&](const S* U) -> S { return small_score<S, NPV>(U, sh, m, p, T, A.r_diag, prof_on ? sprof : nullptr); };
 
   const RunParams rp = *A.run;
   const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
@@ -223,20 +231,35 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
       v = lo + (hi - lo) * u;
       v = v > hi ? hi : v;
     }
-    pop[0][e] = v;
+    popA[e] = v;
   }
   __syncthreads();
   for (int c = tid; c < N; c += nthr)
-    cost[0][c] = A.mode == kSmallResident ? A.cost_io[(size_t)inst * N + c] : score(pop[0] + (size_t)c * pm);
+    costA[c] = A.mode == kSmallResident ? A.cost_io[(size_t)inst * N + c] : score(popA + (size_t)c * pm);
   __syncthreads();
   int sub = 1;
   while (sub < 32 && N * sub * 2 <= nthr) sub <<= 1;
   int cur = 0;
+  // phase timers (EMPC_PHASES): cycles of thread 0 per phase, summed over generations
+  const bool timed = A.dbg != nullptr && inst == 0 && tid == 0;
+  long long ph[5] = {0, 0, 0, 0, 0}, tp = timed ? clock64() : 0;
+  auto mark = [&](int i) {
+    if (timed) {
+      const long long t = clock64();
+      ph[i] += t - tp;
+      tp = t;
+    }
+  };
   for (int g = 0; g < A.evolves; ++g) {
     const int nx = cur ^ 1;
+    S* const pc = cur ? popB : popA;
+    S* const pn = cur ? popA : popB;
+    S* const cc = cur ? costB : costA;
+    S* const cn = cur ? costA : costB;
     // ---- stable selection (K/empc.py:185-188): rank of (ord(cost), row)
-    for (int c = tid; c < N; c += nthr) keys[c] = ord_key(cost[cur][c]);
+    for (int c = tid; c < N; c += nthr) keys[c] = ord_key(cc[c]);
     __syncthreads();
+    mark(0);
     // `sub` lanes (a power of two <= 32) count the rank of one candidate
     for (int base = 0; base < N * sub; base += nthr) {
       const int t = base + tid, c = t / sub, part = t & (sub - 1);
@@ -251,10 +274,11 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
       }
       for (int o = 1; o < sub; o <<= 1) r += __shfl_xor_sync(0xFFFFFFFFu, r, o);
       if (valid && r < K) {
-        for (int q = part; q < pm; q += sub) pop[nx][(size_t)r * pm + q] = pop[cur][(size_t)c * pm + q];
-        if (part == 0) cost[nx][r] = cost[cur][c];
+        for (int q = part; q < pm; q += sub) pn[(size_t)r * pm + q] = pc[(size_t)c * pm + q];
+        if (part == 0) cn[r] = cc[c];
       }
     }
+    mark(1);
     // ---- breeding (K/empc.py:195-204): the per-generation launches' draws
     const uint32_t gen = (uint32_t)(rp.gen0 + g);
     if (nc > 0) {
@@ -266,34 +290,44 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
       }
     }
     __syncthreads();
+    mark(2);
     for (int e = tid; e < nc * pm; e += nthr) {
       const int c = e / pm, q = e % pm, l = q % m;
       S v;
       if (A.inj_parents != nullptr) {
         const size_t gi = (((size_t)g * gridDim.x + inst) * nc + c) * pm + q;
         const bool take = A.inj_take[gi] != 0, mut = A.inj_mut[gi] != 0;
-        const S par = pop[nx][(size_t)src[2 * c + (take ? 1 : 0)] * pm + q];
+        const S par = pn[(size_t)src[2 * c + (take ? 1 : 0)] * pm + q];
         const double nz = mut ? A.inj_noise[gi] * X[SL.sig + l] : 0.0;
         v = (S)((double)par + nz);
       } else {
-        const S par = pop[nx][(size_t)src[2 * c + (tbits[e] ? 1 : 0)] * pm + q];
+        const S par = pn[(size_t)src[2 * c + (tbits[e] ? 1 : 0)] * pm + q];
         v = par + off[q * nc + c];
       }
       const S lo = sUmin[l], hi = sUmax[l];
-      pop[nx][(size_t)(K + c) * pm + q] = v < lo ? lo : (v > hi ? hi : v);
+      pn[(size_t)(K + c) * pm + q] = v < lo ? lo : (v > hi ? hi : v);
     }
     __syncthreads();
-    for (int c = tid; c < nc; c += nthr) cost[nx][K + c] = score(pop[nx] + (size_t)(K + c) * pm);
+    mark(3);
+    for (int c = tid; c < nc; c += nthr) cn[K + c] = score(pn + (size_t)(K + c) * pm);
     __syncthreads();
+    mark(4);
     cur = nx;
   }
+  if (timed) {
+    for (int i = 0; i < 5; ++i) A.dbg[i] = (unsigned long long)ph[i];
+    A.dbg[5] = (unsigned long long)sprof[0];
+    A.dbg[6] = (unsigned long long)sprof[1];
+  }
   // ---- results: population to HBM (the slot), argmin (first NaN, else first minimum)
-  for (int e = tid; e < N * pm; e += nthr) A.pop_io[(size_t)inst * N * pm + e] = pop[cur][e];
-  for (int c = tid; c < N; c += nthr) A.cost_io[(size_t)inst * N + c] = cost[cur][c];
+  S* const pf = cur ? popB : popA;
+  S* const cf = cur ? costB : costA;
+  for (int e = tid; e < N * pm; e += nthr) A.pop_io[(size_t)inst * N * pm + e] = pf[e];
+  for (int c = tid; c < N; c += nthr) A.cost_io[(size_t)inst * N + c] = cf[c];
   uint64_t bo = ~0ull;
   int bi = 0x7FFFFFFF;
   for (int c = tid; c < N; c += nthr) {
-    const S v = cost[cur][c];
+    const S v = cf[c];
     uint64_t o;
     if constexpr (sizeof(S) == 4) o = (v != v) ? 0ull : (uint64_t)ord32((float)v);
     else o = (v != v) ? 0ull : ord64((double)v);
@@ -316,11 +350,11 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   const int best = wi[0];
   double* o = A.out + (size_t)inst * (m + pm + 2);
   for (int q = tid; q < pm; q += nthr) {
-    o[m + q] = (double)pop[cur][(size_t)best * pm + q];
-    if (q < m) o[q] = (double)pop[cur][(size_t)best * pm + q];  // u = first knot (K/empc.py:236)
+    o[m + q] = (double)pf[(size_t)best * pm + q];
+    if (q < m) o[q] = (double)pf[(size_t)best * pm + q];  // u = first knot (K/empc.py:236)
   }
   if (tid == 0) {
-    o[m + pm] = (double)cost[cur][best];
+    o[m + pm] = (double)cf[best];
     o[m + pm + 1] = (double)best;
   }
 }

@@ -33,6 +33,7 @@ struct SmallArgs {
   const uint8_t* inj_take;
   const uint8_t* inj_mut;
   const double* inj_noise;
+  unsigned long long* dbg;  // EMPC_PHASES: [5] cycles of thread 0 per phase (select keys, rank, draws, breed, score)
 };
 
 template <typename S>
