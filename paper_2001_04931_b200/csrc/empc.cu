@@ -684,8 +684,11 @@ class Engine final : public EngineBase {
     int* qin = incremental ? qcount_ + (size_t)((g - 1) & 1) * I_ : nullptr;
     const void* lin = (const char*)qlist_ + (size_t)((g - 1) & 1) * I_ * qcap_ * 2 * sizeof(typename OrdOf<S>::T);
     int* qnext = qcount_ + (size_t)(g & 1) * I_;
+    // radix: every CTA redoes the O(M) threshold search, so only as many CTAs
+    // as the K elite rows need for ranking and copying (16 per CTA)
+    const int rctas = I_ == 1 ? std::max(1, std::min(radix_ctas_ > 0 ? radix_ctas_ : sms_, (d_.K + 15) / 16)) : 1;
     if (use_radix_)
-      launch_ex(select_radix_kernel<S>, dim3(ctas, I_), dim3(1024), radix_select_smem(N, d_.K), pdl_next_, costs, N,
+      launch_ex(select_radix_kernel<S>, dim3(rctas, I_), dim3(1024), radix_select_smem(N, d_.K), pdl_next_, costs, N,
                 d_.K, elite_, incremental, qin, lin, qnext, qcap_, pop_in, pop_out, cost_out, d_.pm);
     else
       launch_ex(select_kernel<S>, dim3(ctas, I_), dim3(256), select_smem_, pdl_next_, costs, N, d_.K, elite_,
@@ -1519,6 +1522,7 @@ class Engine final : public EngineBase {
   size_t cws_n_ = 0;
   size_t select_smem_ = 0;
   bool use_radix_ = false;
+  int radix_ctas_ = std::getenv("EMPC_RADIX_CTAS") ? std::atoi(std::getenv("EMPC_RADIX_CTAS")) : 0;
   bool radix_persist_ok_ = true;  // cleared by EMPC_OPT_RADIX_SELECT = 0
   int radix_min_n_ = 8192;
   bool have_sched_ = false, have_prob_ = false, r_diag_ = true;

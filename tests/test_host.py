@@ -194,3 +194,26 @@ def test_state_bounds_need_a_finite_entry():
         x_max = None
 
     assert not E._has_state_bounds(Dummy())
+
+
+def test_bench_gpus_self_launch(monkeypatch):
+    """`bench.py --gpus N` without a torchrun environment starts N ranks
+    itself (one process per GPU, 127.0.0.1 rendezvous) with the same args."""
+    import importlib
+    import sys
+
+    import bench
+
+    importlib.reload(bench)
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--config", "c5", "--steps", "3"])
+    try:
+        bench.main()
+    except SystemExit as e:
+        assert e.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-6:] == ["--gpus", "4", "--config", "c5", "--steps", "3"]
