@@ -555,8 +555,15 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   }
   EMPC_MARK(8)
   uint8_t* tbits = reinterpret_cast<uint8_t*>(cw_ + 4 * NP + 5 * m);  // crossover choice, 1 byte per gene
-  if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base, true, Off))
+  if (!breed_tile<S>(a, inst, tile0, cnt, tileP, tPS, UsT, src, tbits, cumin, cumax, csig, pop_base, true, Off)) {
+    // a persistent CTA without candidates in this rollout (the init tile of
+    // the last CTAs) still draws its next evolve tile, so that evolve finds
+    // its draws ready like every other CTA
+    if (WS && persist_scratch && a.draw_next && a.draw_cnt > 0)
+      draw_tile<S>(*a.run, (uint32_t)(a.run->gen0 + a.draw_evolve), d.K, d.pm, m, inst, a.cand_base + a.draw_tile0,
+                   a.draw_cnt, tPS, tid, nthr, src, tbits, Off, csig);
     return;
+  }
   __syncthreads();
   EMPC_MARK(3)
 
@@ -1607,9 +1614,7 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
     b.copy_elites = 0;
     b.parents_from_out = s_elite == nullptr ? 1 : 0;  // one-barrier mode: parents via the shared table, from pop_in
     if (s_elite != nullptr) b.elite_idx = s_elite;
-    // the helpers of a CTA without init candidates never ran (it returned
-    // early), so its first evolve draws inline
-    b.draws_ready = P.predraw && (g > 0 || (int)blockIdx.x * a.tile < a.nc);
+    b.draws_ready = P.predraw;  // (CTAs without init candidates drew theirs at the early return)
     b.draw_next = P.predraw && g + 1 < P.evolves;
     b.draw_evolve = g + 1;
     b.pop_in = P.pop[cur];

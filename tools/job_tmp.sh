@@ -1,2 +1,4 @@
-for r in 0 32 148; do EMPC_RADIX_CTAS=$r python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && EMPC_RADIX_CTAS=$r ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/l4_$r.csv python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; done
-python tools/sweep.py c4 '' 'EMPC_RADIX_CTAS=32' 'EMPC_RADIX_CTAS=148'
+EMPC_PHASES=1 timeout 120 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 >/dev/null | grep -E "timeline" | tail -1
+python tools/sweep.py c3 '' ''
+for G in 2 3; do timeout 120 python tools/dbg_ws.py $G | tail -1; done
+timeout 1200 python -m pytest tests -q -m gpu --timeout 600 2>&1 | tail -1
