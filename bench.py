@@ -66,6 +66,8 @@ def parse():
                          "population-sharding scaling curve")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="CPU baseline budget (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l2", default="flush", choices=["flush", "warm"],
+                    help="warm: no L2 flush between timed solves (experiment only; the line says so)")
     ap.add_argument("--tensor-cores", default="auto", choices=["auto", "on", "off"],
                     help="FP32 rollout recursion on the tcgen05 tensor cores (TF32 split precision): auto = where it "
                          "measured faster (DESIGN.md §4.8)")
@@ -421,12 +423,12 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    ms_each, _, nroll, nlaunch = time_device(args.steps)
+    ms_each, _, nroll, nlaunch = time_device(args.steps, flush=0 if args.l2 == "warm" else 1)
     torch.cuda.synchronize()
     clocks = sampler.stop()
     total_ms = sum(ms_each)
     # roofline pass: per-launch rollout durations (events around each launch)
-    _, rollout_ms, _, _ = time_device(min(args.steps, 20), want_rollout=True)
+    _, rollout_ms, _, _ = time_device(min(args.steps, 20), flush=0 if args.l2 == "warm" else 1, want_rollout=True)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -556,7 +558,9 @@ def run_ours(args):
         "dtype": "f32" if not condensed else "f32 population, f64 quadratic form", "scorer": args.scorer, "data": "synthetic (reference recipe: linearized N-link arms, SURVEY §8d)",
         "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}", "dof": w.dof, "T": w.T, "p": w.p,
                    "N": w.N, "K": w.K, "G": w.G, "instances": w_total.instances,
-                   "instances_per_rank": w.instances, "l2": "flushed (256 MiB write) between timed solves",
+                   "instances_per_rank": w.instances,
+                   "l2": "flushed (256 MiB write) between timed solves" if args.l2 == "flush"
+                   else "NOT flushed (experiment: warm L2)",
                    "kernel_variant": ctx.h.describe()},
         "latency_ms": {"median": statistics.median(ms_each), "q1": float(np.percentile(ms_each, 25)),
                        "q3": float(np.percentile(ms_each, 75)), "min": min(ms_each)},

@@ -775,7 +775,7 @@ class Engine final : public EngineBase {
     a.elite_idx = elite_; a.run = run_d_;
     a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
     if (phases_ && (size_t)grid * 16 + 32 <= dbg_n_) {
-      CK(cudaMemsetAsync(dbg_, 0, ((size_t)grid * 16 + 32) * 8, stream_));
+      CK(cudaMemsetAsync(dbg_, 0, ((size_t)grid * 16 + 48) * 8, stream_));
       a.dbg = dbg_;
       dbg_ctas_ = grid;
     }
@@ -1212,7 +1212,7 @@ class Engine final : public EngineBase {
                      acc[0], acc[1], acc[2], acc[3], acc[4]);
         dbg_ctas_ = 0;
       }
-      // persistent kernel: the last generation's selection (marks 13-15)
+      // persistent kernel: the selection before the recorded evolve (marks 13-15)
       double w1 = 0, w2 = 0, w3 = 0;
       int cnt = 0;
       for (int c = 0; c < dbg_ctas_; ++c) {
@@ -1232,6 +1232,13 @@ class Engine final : public EngineBase {
         for (int g = 2; g < 30 && gt[g] > gt[0]; ++g) std::fprintf(stderr, " gen%d_end=%.2f", g - 1, (gt[g] - gt[0]) * 1e-3);
         if (gt[31] > gt[0]) std::fprintf(stderr, " end=%.2f", (gt[31] - gt[0]) * 1e-3);
         std::fprintf(stderr, "\n");
+        std::vector<unsigned long long> rm(16);  // first (radix) selection, CTA 0
+        CK(cudaMemcpy(rm.data(), dbg_ + (size_t)dbg_ctas_ * 16 + 32, 16 * 8, cudaMemcpyDeviceToHost));
+        if (rm[0] != 0) {
+          std::fprintf(stderr, "first selection (us, CTA 0, from the key load): common_bits=%.2f", (rm[1] - rm[0]) * 1e-3);
+          for (int q = 2; q < 10 && rm[q] != 0; ++q) std::fprintf(stderr, " pass%d=%.2f", q - 1, (rm[q] - rm[0]) * 1e-3);
+          std::fprintf(stderr, " compact=%.2f ranked=%.2f\n", (rm[10] - rm[0]) * 1e-3, (rm[11] - rm[0]) * 1e-3);
+        }
       }
     }
   }

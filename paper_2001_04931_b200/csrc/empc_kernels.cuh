@@ -1027,66 +1027,101 @@ __device__ __forceinline__ void block_exclusive_scan(int& v, int* warp_tot, int&
   __syncthreads();
 }
 
+// Radix-select helpers.  Bits all keys share are skipped: the block AND / OR
+// of the keys gives the highest differing bit, where the first digit starts
+// (a population whose costs share sign and exponent bits would otherwise
+// spend a pass on one hot bin).
+__device__ __forceinline__ void radix_common_bits(unsigned long long kand, unsigned long long kor, int* aux,
+                                                  int& hb, unsigned long long& prefix, unsigned long long& mask) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned ah = __reduce_and_sync(0xFFFFFFFFu, (unsigned)(kand >> 32));
+  const unsigned al = __reduce_and_sync(0xFFFFFFFFu, (unsigned)kand);
+  const unsigned oh = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(kor >> 32));
+  const unsigned ol = __reduce_or_sync(0xFFFFFFFFu, (unsigned)kor);
+  if (tid == 0) {
+    aux[36] = -1; aux[37] = -1; aux[38] = 0; aux[39] = 0;
+  }
+  __syncthreads();
+  if (lane == 0) {
+    atomicAnd(&aux[36], (int)ah); atomicAnd(&aux[37], (int)al);
+    atomicOr(&aux[38], (int)oh); atomicOr(&aux[39], (int)ol);
+  }
+  __syncthreads();
+  kand = ((unsigned long long)(unsigned)aux[36] << 32) | (unsigned)aux[37];
+  kor = ((unsigned long long)(unsigned)aux[38] << 32) | (unsigned)aux[39];
+  const unsigned long long diff = kand ^ kor;
+  hb = diff == 0ull ? 0 : 63 - __clzll(diff);
+  mask = hb >= 63 ? 0ull : (~0ull << (hb + 1));
+  prefix = kand & mask;
+}
+
+// After a digit histogram: the bucket holding the krem-th key (warp 0, 8 bins
+// per lane); updates prefix / mask / krem, done when the bucket is taken whole.
+__device__ __forceinline__ void radix_pick_bucket(const int* hist, int* aux, int shift, int& krem,
+                                                  unsigned long long& prefix, unsigned long long& mask, bool& done) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __syncthreads();
+  if (warp == 0) {
+    int loc[8], s8 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { loc[q] = hist[lane * 8 + q]; s8 += loc[q]; }
+    int inc = s8;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int before = inc - s8;
+    if (before < krem && krem <= inc) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (before < krem && krem <= before + loc[q]) {
+          aux[32] = lane * 8 + q;
+          aux[33] = krem - before;
+          aux[34] = loc[q];
+        }
+        before += loc[q];
+      }
+    }
+  }
+  __syncthreads();
+  const int b = aux[32];
+  krem = aux[33];
+  // near the bottom the digit overlaps decided bits, which are constant over
+  // the keys matching the prefix
+  prefix |= (unsigned long long)b << shift;
+  mask |= 255ull << shift;
+  done = aux[34] == krem;
+  __syncthreads();
+}
+
 // The K smallest of M unique 64-bit keys in shared memory: 8-bit radix
-// select of the K-th key (warp-aggregated histograms, early exit when the
-// bucket is taken whole), then a deterministic compaction of the keys <= it
+// select of the K-th key, then a deterministic compaction of the keys <= it
 // into E in key-position order (block scan).  total = number compacted
 // (min(K, M)).  All threads of the block call it.
 __device__ __forceinline__ void radix_topk_compact(const unsigned long long* keys, int M, int K,
                                                    unsigned long long* E, int* hist, int* aux, int& total) {
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
-  // ---- radix select of the K-th smallest key: prefix / mask of the bucket
-  unsigned long long prefix = 0ull, mask = 0ull;
+  unsigned long long kand = ~0ull, kor = 0ull;
+  for (int j = tid; j < M; j += nthr) {
+    const unsigned long long k = keys[j];
+    kand &= k;
+    kor |= k;
+  }
+  int hb;
+  unsigned long long prefix, mask;
+  radix_common_bits(kand, kor, aux, hb, prefix, mask);
   int krem = K;
   bool done = K >= M;
-  for (int shift = 56; shift >= 0 && !done; shift -= 8) {
+  for (int top = hb; top >= 0 && !done; top -= 8) {
+    const int shift = top >= 7 ? top - 7 : 0;  // digit = bits [shift, shift + 8)
     for (int b = tid; b < 256; b += nthr) hist[b] = 0;
     __syncthreads();
-    // warp-aggregated histogram: costs of a converging population share
-    // their top bytes, so plain shared atomics would serialise on one bin
-    for (int j0 = warp * 32; j0 < M; j0 += nwarps * 32) {
-      const int j = j0 + lane;
-      int bin = 256;
-      if (j < M) {
-        const unsigned long long k = keys[j];
-        if ((k & mask) == prefix) bin = (int)((k >> shift) & 255ull);
-      }
-      const unsigned same = __match_any_sync(0xFFFFFFFFu, bin);
-      if (bin < 256 && lane == __ffs(same) - 1) atomicAdd(&hist[bin], __popc(same));
+    for (int j = tid; j < M; j += nthr) {
+      const unsigned long long k = keys[j];
+      if ((k & mask) == prefix) atomicAdd(&hist[(int)((k >> shift) & 255ull)], 1);
     }
-    __syncthreads();
-    if (warp == 0) {
-      // bucket holding the krem-th key: prefix sums of the 256 bins, 8 per lane
-      int loc[8], s8 = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) { loc[q] = hist[lane * 8 + q]; s8 += loc[q]; }
-      int inc = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      int before = inc - s8;
-      if (before < krem && krem <= inc) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (before < krem && krem <= before + loc[q]) {
-            aux[32] = lane * 8 + q;
-            aux[33] = krem - before;
-            aux[34] = loc[q];
-          }
-          before += loc[q];
-        }
-      }
-    }
-    __syncthreads();
-    const int b = aux[32];
-    krem = aux[33];
-    prefix |= (unsigned long long)b << shift;
-    mask |= 255ull << shift;
-    done = aux[34] == krem;  // the whole bucket is below the threshold
-    __syncthreads();
+    radix_pick_bucket(hist, aux, shift, krem, prefix, mask, done);
   }
   // elites: keys below the bucket, plus the bucket when it is taken whole
   // (the loop ends with exactly K keys <= thr)
@@ -1102,13 +1137,57 @@ __device__ __forceinline__ void radix_topk_compact(const unsigned long long* key
   __syncthreads();
 }
 
+// Register-resident variant (M <= R * blockDim.x): thread t holds keys
+// t + i * blockDim.x in kr[i], so the digit passes issue independent shared
+// atomics with no shared loads in between.  E is filled in thread-major order
+// (the same on every CTA: only the set matters to the ranking).
+template <int R>
+__device__ __forceinline__ void radix_topk_regs(const unsigned long long (&kr)[R], int M, int K,
+                                                unsigned long long* E, int* hist, int* aux, int& total,
+                                                unsigned long long* mk = nullptr) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  unsigned long long kand = ~0ull, kor = 0ull;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (tid + i * nthr < M) {
+      kand &= kr[i];
+      kor |= kr[i];
+    }
+  int hb;
+  unsigned long long prefix, mask;
+  radix_common_bits(kand, kor, aux, hb, prefix, mask);
+  if (mk != nullptr && tid == 0) mk[0] = gtimer();
+  int krem = K;
+  bool done = K >= M;
+  for (int top = hb; top >= 0 && !done; top -= 8) {
+    const int shift = top >= 7 ? top - 7 : 0;
+    for (int b = tid; b < 256; b += nthr) hist[b] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (tid + i * nthr < M && (kr[i] & mask) == prefix) atomicAdd(&hist[(int)((kr[i] >> shift) & 255ull)], 1);
+    radix_pick_bucket(hist, aux, shift, krem, prefix, mask, done);
+    if (mk != nullptr && tid == 0 && (hb - top) / 8 < 7) mk[1 + (hb - top) / 8] = gtimer();
+  }
+  const unsigned long long thr = K >= M ? ~0ull : (prefix | ~mask);
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) cnt += (tid + i * nthr < M && kr[i] <= thr) ? 1 : 0;
+  block_exclusive_scan(cnt, aux, total);
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (tid + i * nthr < M && kr[i] <= thr) E[cnt++] = kr[i];
+  __syncthreads();
+}
+
 template <typename S>
 __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
                                                   int incremental, int* __restrict__ qcount_in,
                                                   const void* __restrict__ qlist_in, int* __restrict__ qcount_next,
                                                   int qcap, const S* __restrict__ pop_in, S* __restrict__ pop_out,
                                                   S* __restrict__ cost_out, int pm, int* s_elite = nullptr,
-                                                  unsigned long long* fold_amin = nullptr) {
+                                                  unsigned long long* fold_amin = nullptr,
+                                                  unsigned long long* mk = nullptr) {
   static_assert(sizeof(S) == 4, "64-bit (ord32, row) keys: FP32 costs");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
@@ -1131,15 +1210,39 @@ __device__ __forceinline__ void select_radix_body(const S* __restrict__ costs, i
   if (blockIdx.x == 0 && tid == 0 && qcount_next != nullptr) qcount_next[inst] = 0;
   pdl_trigger();
   const uint32_t* ql = full ? nullptr : reinterpret_cast<const uint32_t*>(qlist_in) + (size_t)inst * qcap * 2;
-  for (int j = tid; j < M; j += nthr) {
-    unsigned long long k;
-    if (j < K || full) k = ((unsigned long long)ord32((float)c[j]) << 32) | (unsigned)j;
-    else k = ((unsigned long long)ql[2 * (j - K)] << 32) | ql[2 * (j - K) + 1];
-    keys[j] = k;
-  }
   int total;
-  radix_topk_compact(keys, M, K, E, hist, aux, total);
+  constexpr int kRegKeys = 16;
+  if (M <= kRegKeys * nthr) {
+    // keys in registers, loaded straight from the costs / qualifier list (the
+    // costs were written by other CTAs before the grid barrier: L2 loads)
+    unsigned long long kr[kRegKeys];
+#pragma unroll
+    for (int i = 0; i < kRegKeys; ++i) {
+      const int j = tid + i * nthr;
+      kr[i] = ~0ull;
+      if (j < M) {
+        if (j < K || full) kr[i] = ((unsigned long long)ord32((float)__ldcg(c + j)) << 32) | (unsigned)j;
+        else kr[i] = ((unsigned long long)__ldcg(ql + 2 * (j - K)) << 32) | __ldcg(ql + 2 * (j - K) + 1);
+      }
+    }
+    if (mk != nullptr && tid == 0) mk[0] = gtimer();
+    radix_topk_regs<kRegKeys>(kr, M, K, E, hist, aux, total, mk != nullptr ? mk + 1 : nullptr);
+  } else {
+    for (int j = tid; j < M; j += nthr) {
+      unsigned long long k;
+      if (j < K || full) k = ((unsigned long long)ord32((float)c[j]) << 32) | (unsigned)j;
+      else k = ((unsigned long long)ql[2 * (j - K)] << 32) | ql[2 * (j - K) + 1];
+      keys[j] = k;
+    }
+    __syncthreads();
+    radix_topk_compact(keys, M, K, E, hist, aux, total);
+  }
+  if (mk != nullptr && tid == 0) mk[10] = gtimer();
   const int ne = min(K, total);
+  struct MarkEnd {  // mk[11]: end of the ranking / carry-over of this CTA's slice
+    unsigned long long* m;
+    __device__ ~MarkEnd() { if (m != nullptr && threadIdx.x == 0) m[11] = gtimer(); }
+  } mark_end{mk};
   if (s_elite != nullptr) {
     // redundant mode (one grid barrier per generation): every CTA ranks ALL
     // K elites into its own shared rank -> row table (K^2 comparisons), then
@@ -1565,9 +1668,12 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
   if (s_elite != nullptr && blockIdx.x == 0 && threadIdx.x == 0) P.qcount[0] = 0;
   for (int g = 0; g < P.evolves; ++g) {
     if (gt && g > 0 && g + 1 < 30) gt[g + 1] = gtimer();
-    EMPC_MARK(13)
+    // selection marks 13-15 of the evolve the rollout marks record
+    const bool mark = a.dbg != nullptr && threadIdx.x == 0 && (P.dbg_gen < 0 || g == P.dbg_gen);
+    unsigned long long* const mk = mark ? a.dbg + (size_t)blockIdx.x * 16 : nullptr;
+    if (mk) mk[13] = gtimer();
     grid.sync();
-    EMPC_MARK(14)
+    if (mk) mk[14] = gtimer();
     const int inc = (g > 0 && P.incremental) ? 1 : 0;
     if constexpr (sizeof(S) == 4) {
       if (s_elite != nullptr) {
@@ -1583,7 +1689,8 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
         // which needs fewer passes and barriers
         select_radix_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
                              (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap,
-                             P.pop[cur], P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
+                             P.pop[cur], P.pop[cur ^ 1], P.cost[cur ^ 1], pm, nullptr, nullptr,
+                             gt != nullptr ? gt + 32 : nullptr);
       } else {
         select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
                        (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
@@ -1594,7 +1701,7 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
                      (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
                      P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
     }
-    EMPC_MARK(15)
+    if (mk) mk[15] = gtimer();
     if (s_elite == nullptr) grid.sync();
     RolloutArgs<S> b = a;
     b.mode = P.inj_parents != nullptr ? kBreedInject : kBreedPhilox;

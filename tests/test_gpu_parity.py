@@ -570,3 +570,36 @@ def test_radix_selection_solve_equals_counting_selection():
     ctx.h.set_option(nat.EMPC_OPT_RADIX_SELECT, 1)
     for a, b in zip(out[0], out[1]):
         np.testing.assert_array_equal(a, b)
+
+
+def _structured_costs(kind, N, rng):
+    if kind == "equal":  # keys differ in the row bits only
+        return np.full(N, 3.25)
+    if kind == "ulps":  # costs a few float32 ulps apart
+        base = np.array([1234.5], np.float32).view(np.uint32)[0]
+        return (base + rng.integers(0, 4, N).astype(np.uint32)).view(np.float32).astype(np.float64)
+    if kind == "two":
+        return rng.choice([1.0, 2.0], N)
+    # magnitudes over many binades, both signs, zeros and infinities
+    c = rng.standard_normal(N) * 10.0 ** rng.uniform(-30, 30, N)
+    c[:: max(1, N // 7)] = 0.0
+    c[1::11] = -0.0
+    c[2] = np.inf
+    return c.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("N,K", [(100, 6), (4096, 256), (16384, 1024), (20000, 999)])
+@pytest.mark.parametrize("kind", ["equal", "ulps", "two", "spread"])
+def test_radix_selection_structured_costs(N, K, kind):
+    """Radix select forced on (register-resident keys up to 16 per thread,
+    shared-memory keys beyond): the common-bit skip and the digits that
+    overlap decided bits near the bottom must keep argsort(kind="stable")."""
+    rng = np.random.default_rng(N * 7 + len(kind))
+    costs = _structured_costs(kind, N, rng)
+    ctx = P.empc._Context(2, 1, 5, 2, N, K, 1, False, "fp32")  # private: the option stays local
+    ctx.h.set_option(nat.EMPC_OPT_RADIX_SELECT, 1)
+    elite = np.empty(K, np.int32)
+    best = np.empty(1, np.int32)
+    ctx.h.call("empc_select", nat.dptr(nat.f64(costs)), nat.iptr(elite), nat.iptr(best))
+    np.testing.assert_array_equal(elite, np.argsort(costs, kind="stable")[:K])
+    assert int(best[0]) == int(np.argmin(costs))
