@@ -31,6 +31,50 @@ using namespace empc;
 
 namespace {
 
+// Byte-range copies by one kernel (16-byte words when a range allows it).
+// The public-API graph moves its inputs and outputs with these instead of
+// DMA nodes: the staging upload reads the mapped pinned host buffers, the
+// result is stored straight into mapped pinned memory, the output slot is a
+// device copy.  Each DMA node costs ~5 us of graph latency
+// (tools/graph_io_probe.cu: 33.7 -> 17.5 us around an empty kernel).
+struct CopySpan {
+  const void* src;
+  void* dst;
+  size_t bytes;
+};
+struct CopySpans {
+  CopySpan s[3];
+  int n = 0;
+  void add(const void* src, void* dst, size_t bytes) { s[n++] = CopySpan{src, dst, bytes}; }
+  size_t largest() const {
+    size_t b = 0;
+    for (int k = 0; k < n; ++k) b = std::max(b, s[k].bytes);
+    return b;
+  }
+};
+__global__ void copy_spans_kernel(const CopySpans c) {
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  for (int k = 0; k < c.n; ++k) {
+    const CopySpan sp = c.s[k];
+    const uintptr_t al = (uintptr_t)sp.src | (uintptr_t)sp.dst | (uintptr_t)sp.bytes;
+    if ((al & 15) == 0) {
+      const uint4* a = static_cast<const uint4*>(sp.src);
+      uint4* b = static_cast<uint4*>(sp.dst);
+      for (size_t i = tid; i < sp.bytes / 16; i += nt) b[i] = a[i];
+    } else if ((al & 7) == 0) {
+      const uint2* a = static_cast<const uint2*>(sp.src);
+      uint2* b = static_cast<uint2*>(sp.dst);
+      for (size_t i = tid; i < sp.bytes / 8; i += nt) b[i] = a[i];
+    } else {
+      const unsigned char* a = static_cast<const unsigned char*>(sp.src);
+      unsigned char* b = static_cast<unsigned char*>(sp.dst);
+      for (size_t i = tid; i < sp.bytes; i += nt) b[i] = a[i];
+    }
+  }
+}
+// host-memory spans above this size stay DMA copies (C5 stages 110 MB)
+constexpr size_t kZeroCopyMax = (size_t)1 << 20;
+
 thread_local std::string g_create_error;
 
 constexpr int kMaxSmem = 227 * 1024;
@@ -159,6 +203,10 @@ class Engine final : public EngineBase {
     out_stride_ = d_.m + d_.pm + 2;
     CK(cudaMalloc(&out_d_, sizeof(double) * (size_t)I_ * out_stride_));
     CK(cudaMallocHost(&out_h_, sizeof(double) * (size_t)I_ * out_stride_));
+    // device views of the pinned staging / result buffers (zero-copy IO of the public-API graph)
+    CK(cudaHostGetDevicePointer((void**)&stage_prob_hd_, stage_prob_h_, 0));
+    CK(cudaHostGetDevicePointer((void**)&stage_state_hd_, stage_state_h_, 0));
+    CK(cudaHostGetDevicePointer((void**)&out_hd_, out_h_, 0));
     CK(cudaMalloc(&idx1_, sizeof(int) * d_.T));
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
     CK(cudaMalloc(&seg_, sizeof(int) * d_.T));
@@ -965,17 +1013,47 @@ class Engine final : public EngineBase {
     if (copies) enqueue_h2d();
     if (!r.init) {
       Slot& s = slot(r.slot_in);
-      CK(cudaMemcpyAsync(pop_[0], s.cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice, stream_));
-      CK(cudaMemcpyAsync(cost_[0], s.costs, sizeof(S) * (size_t)I_ * d_.N, cudaMemcpyDeviceToDevice, stream_));
+      CopySpans c;
+      c.add(s.cands, pop_[0], sizeof(S) * (size_t)I_ * d_.N * d_.pm);
+      c.add(s.costs, cost_[0], sizeof(S) * (size_t)I_ * d_.N);
+      launch_copies(c);
     }
   }
 
   void enqueue_h2d() {
-    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, sizeof(double) * (size_t)I_ * SL_.stride, cudaMemcpyHostToDevice,
-                       stream_));
+    const size_t prob_bytes = sizeof(double) * (size_t)I_ * SL_.stride;
     const size_t state_bytes =
         reinterpret_cast<uintptr_t>(run_h_ + 1) - reinterpret_cast<uintptr_t>(stage_state_h_);
+    if (prob_bytes + state_bytes <= kZeroCopyMax) {
+      CopySpans c;
+      c.add(stage_prob_hd_, stage_prob_d_, prob_bytes);
+      c.add(stage_state_hd_, stage_state_d_, state_bytes);
+      launch_copies(c);
+      return;
+    }
+    CK(cudaMemcpyAsync(stage_prob_d_, stage_prob_h_, prob_bytes, cudaMemcpyHostToDevice, stream_));
     CK(cudaMemcpyAsync(stage_state_d_, stage_state_h_, state_bytes, cudaMemcpyHostToDevice, stream_));
+  }
+
+  void launch_copies(const CopySpans& c) {
+    if (c.n == 0) return;
+    const size_t words = (c.largest() + 15) / 16;
+    const int ctas = (int)std::max<size_t>(1, std::min<size_t>((size_t)sms_ * 4, (words + 255) / 256));
+    copy_spans_kernel<<<ctas, 256, 0, stream_>>>(c);
+    CK(cudaGetLastError());
+  }
+
+  // result download + copy of the final population into the output slot
+  void enqueue_outputs(int cur, const Slot* so) {
+    const size_t out_bytes = sizeof(double) * (size_t)I_ * out_stride_;
+    CopySpans c;
+    if (out_bytes <= kZeroCopyMax) c.add(out_d_, out_hd_, out_bytes);
+    else CK(cudaMemcpyAsync(out_h_, out_d_, out_bytes, cudaMemcpyDeviceToHost, stream_));
+    if (so != nullptr) {
+      c.add(pop_[cur], so->cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm);
+      c.add(cost_[cur], so->costs, sizeof(S) * (size_t)I_ * d_.N);
+    }
+    launch_copies(c);
   }
 
   using GKey = std::tuple<bool, bool, int, int, bool, int, int, int, int, bool, int, bool, int>;
@@ -1004,15 +1082,7 @@ class Engine final : public EngineBase {
     try {
       if (io) enqueue_h2d();
       cur = enqueue_core(r, nullptr);
-      if (io) {
-        CK(cudaMemcpyAsync(out_h_, out_d_, sizeof(double) * (size_t)I_ * out_stride_, cudaMemcpyDeviceToHost, stream_));
-        if (slot_captured(r)) {
-          Slot& so = slot(r.slot_out);
-          CK(cudaMemcpyAsync(so.cands, pop_[cur], sizeof(S) * (size_t)I_ * d_.N * d_.pm, cudaMemcpyDeviceToDevice,
-                             stream_));
-          CK(cudaMemcpyAsync(so.costs, cost_[cur], sizeof(S) * (size_t)I_ * d_.N, cudaMemcpyDeviceToDevice, stream_));
-        }
-      }
+      if (io) enqueue_outputs(cur, slot_captured(r) ? &slot(r.slot_out) : nullptr);
     } catch (...) {
       cudaStreamEndCapture(stream_, &g);
       throw;
@@ -1510,6 +1580,7 @@ class Engine final : public EngineBase {
   void* qlist_ = nullptr;
   int qcap_ = 0;
   double *out_d_ = nullptr, *out_h_ = nullptr;
+  double *stage_prob_hd_ = nullptr, *stage_state_hd_ = nullptr, *out_hd_ = nullptr;  // device views of pinned memory
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
   unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key
