@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <stdexcept>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -175,6 +176,7 @@ class Engine final : public EngineBase {
     SL_.umin = s; s += m;
     SL_.umax = s; s += m;
     SL_.stride = s + (s & 1);  // even: every instance's block starts 16-byte aligned (async staging copies)
+    if (SL_.stride != stage_stride(n, m)) throw std::logic_error("staging layout and stage_stride disagree");
     SL_.x0 = 0;
     SL_.sig = n;
     SL_.sstride = n + m;
@@ -207,6 +209,8 @@ class Engine final : public EngineBase {
     CK(cudaHostGetDevicePointer((void**)&stage_prob_hd_, stage_prob_h_, 0));
     CK(cudaHostGetDevicePointer((void**)&stage_state_hd_, stage_state_h_, 0));
     CK(cudaHostGetDevicePointer((void**)&out_hd_, out_h_, 0));
+    run_hd_ = reinterpret_cast<RunParams*>(reinterpret_cast<char*>(stage_state_hd_) +
+                                           (reinterpret_cast<char*>(run_h_) - reinterpret_cast<char*>(stage_state_h_)));
     CK(cudaMalloc(&idx1_, sizeof(int) * d_.T));
     CK(cudaMalloc(&idx2_, sizeof(int) * d_.T));
     CK(cudaMalloc(&seg_, sizeof(int) * d_.T));
@@ -877,16 +881,20 @@ class Engine final : public EngineBase {
   // Small problems (C1): the whole solve in one CTA per instance with the
   // population resident in shared memory (empc_small.cu).  Auto: n <= 8, a
   // diagonal Q, the rollout scorer and little work per generation.
-  template <typename Pre, typename Post>
-  bool try_small(const empc_run_args& r, bool timed, Pre& pre, Post& post, const std::vector<const void*>* inj) {
+  bool small_eligible() const {
     if (small_mode_ == 0 || scorer_ != 0 || dense_ || cps_ > 0 || (forced_ >= 0 && small_mode_ < 1)) return false;
-    const SmallKernel<S> kern = small_kernel<S>(d_.n);
-    if (kern == nullptr || d_.N > 4096) return false;
-    const size_t smem = small_smem<S>(d_.n, d_.m, d_.T, d_.p, d_.N, d_.K);
-    if (smem > (size_t)kMaxSmem) return false;
+    if (small_kernel<S>(d_.n) == nullptr || d_.N > 4096) return false;
+    if (small_smem<S>(d_.n, d_.m, d_.T, d_.p, d_.N, d_.K) > (size_t)kMaxSmem) return false;
     const int npv = d_.n <= 4 ? 4 : 8;
     const long long work = (long long)d_.N * d_.T * npv * npv;
-    if (small_mode_ < 0 && work > (1LL << 18)) return false;
+    return !(small_mode_ < 0 && work > (1LL << 18));
+  }
+
+  template <typename Pre, typename Post>
+  bool try_small(const empc_run_args& r, bool timed, Pre& pre, Post& post, const std::vector<const void*>* inj) {
+    if (!small_eligible()) return false;
+    const SmallKernel<S> kern = small_kernel<S>(d_.n);
+    const size_t smem = small_smem<S>(d_.n, d_.m, d_.T, d_.p, d_.N, d_.K);
     if (!small_attr_set_) {
       CK(cudaFuncSetAttribute(small_kernel<S>(4), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
       CK(cudaFuncSetAttribute(small_kernel<S>(8), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -896,7 +904,19 @@ class Engine final : public EngineBase {
     A.d = d_; A.SL = SL_; A.evolves = r.evolves; A.r_diag = r_diag_ ? 1 : 0;
     A.prob = stage_prob_d_; A.state = stage_state_d_; A.run = run_d_;
     A.idx1 = idx1_; A.idx2 = idx2_; A.seg = seg_; A.cw = cw_; A.G = G_;
+    A.pop_in = pop_[0]; A.cost_in = cost_[0];
     A.pop_io = pop_[0]; A.cost_io = cost_[0]; A.out = out_d_;
+    if (io_direct_) {
+      // public-API graph: staging read from the mapped pinned buffers, the
+      // result stored into mapped pinned memory, the population written
+      // straight into the output slot (captured slots; others are copied
+      // from pop_[0] after the graph)
+      A.prob = stage_prob_hd_; A.state = stage_state_hd_; A.run = run_hd_; A.out = out_hd_;
+      if (slot_captured(r)) {
+        Slot& so = slot(r.slot_out);
+        A.pop_io = so.cands; A.cost_io = so.costs;
+      }
+    }
     A.mode = r.init ? kInitPhilox : (r.rescore ? kScore : kSmallResident);
     if (inj && r.init) {
       A.inj_init = (const S*)(*inj)[0];
@@ -1080,10 +1100,15 @@ class Engine final : public EngineBase {
     CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     int cur = 0;
     try {
-      if (io) enqueue_h2d();
+      // the resident small solve moves its own inputs / outputs
+      const bool direct = io && small_eligible();
+      if (io && !direct) enqueue_h2d();
+      io_direct_ = direct;
       cur = enqueue_core(r, nullptr);
-      if (io) enqueue_outputs(cur, slot_captured(r) ? &slot(r.slot_out) : nullptr);
+      io_direct_ = false;
+      if (io && !direct) enqueue_outputs(cur, slot_captured(r) ? &slot(r.slot_out) : nullptr);
     } catch (...) {
+      io_direct_ = false;
       cudaStreamEndCapture(stream_, &g);
       throw;
     }
@@ -1581,6 +1606,8 @@ class Engine final : public EngineBase {
   int qcap_ = 0;
   double *out_d_ = nullptr, *out_h_ = nullptr;
   double *stage_prob_hd_ = nullptr, *stage_state_hd_ = nullptr, *out_hd_ = nullptr;  // device views of pinned memory
+  RunParams* run_hd_ = nullptr;
+  bool io_direct_ = false;  // the small solve moves the public-API graph's inputs / outputs itself
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
   unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key

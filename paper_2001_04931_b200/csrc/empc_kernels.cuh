@@ -89,6 +89,14 @@ struct RolloutArgs {
   unsigned long long* amin; // last generation of the persistent solve: argmin key of the population
 };
 
+// doubles per instance in the problem staging block [Ad | Bd | wd | Q | R |
+// x_goal | u_goal | u_min | u_max], padded even (16-byte aligned blocks);
+// the layout is StageLayout (set by the engine)
+__host__ __device__ inline int stage_stride(int n, int m) {
+  const int s = 2 * n * n + n * m + 2 * n + m * m + 3 * m;
+  return s + (s & 1);
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

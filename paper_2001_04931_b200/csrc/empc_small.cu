@@ -22,7 +22,6 @@ struct SmallShared {
 
 template <typename S>
 __host__ __device__ inline size_t small_smem_bytes(int n, int m, int T, int p, int N, int K) {
-  (void)n;
   const int pm = p * m, nc = N - K;
   const int NPV = n <= 4 ? 4 : 8;
   size_t b = 0;
@@ -39,6 +38,8 @@ __host__ __device__ inline size_t small_smem_bytes(int n, int m, int T, int p, i
   b += al((size_t)nc * 2 * sizeof(int));            // parent ranks
   b += al((size_t)nc * pm);                         // crossover bits
   b += al((size_t)nc * pm * sizeof(S));             // mutation offsets
+  b += al((size_t)stage_stride(n, m) * sizeof(double));   // problem staging block
+  b += al((size_t)(n + m) * sizeof(double));              // x0, sigma
   return b + 64;
 }
 
@@ -133,8 +134,6 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   const int inst = blockIdx.x;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const StageLayout& SL = A.SL;
-  const double* __restrict__ P = A.prob + (size_t)inst * SL.stride;
-  const double* __restrict__ X = A.state + (size_t)inst * SL.sstride;
   auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
   unsigned char* ptr = smem_raw;
   S* sD = reinterpret_cast<S*>(ptr); ptr += al((size_t)NPV * NPV * sizeof(S));
@@ -163,9 +162,23 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   OT* keys = reinterpret_cast<OT*>(ptr); ptr += al((size_t)(N > 64 ? N : 64) * 8);
   int* src = reinterpret_cast<int*>(ptr); ptr += al((size_t)nc * 2 * sizeof(int));
   uint8_t* tbits = reinterpret_cast<uint8_t*>(ptr); ptr += al((size_t)nc * pm);
-  S* off = reinterpret_cast<S*>(ptr);
+  S* off = reinterpret_cast<S*>(ptr); ptr += al((size_t)nc * pm * sizeof(S));
+  double* const sP = reinterpret_cast<double*>(ptr); ptr += al((size_t)SL.stride * sizeof(double));
+  double* const sX = reinterpret_cast<double*>(ptr);
 
-  // ---- stage the problem (error coordinates, as the rollout kernel)
+  // ---- the instance's staging blocks into shared memory in one parallel
+  // pass (they may live in mapped host memory), then the problem in error
+  // coordinates, as the rollout kernel
+  {
+    const double* gp = A.prob + (size_t)inst * SL.stride;
+    const double* gx = A.state + (size_t)inst * SL.sstride;
+    for (int e = tid; e < SL.stride; e += nthr) sP[e] = gp[e];
+    for (int e = tid; e < n + m; e += nthr) sX[e] = gx[e];
+  }
+  const RunParams rp = *A.run;
+  __syncthreads();
+  const double* __restrict__ P = sP;
+  const double* __restrict__ X = sX;
   for (int e = tid; e < NPV * NPV; e += nthr) {
     const int i = e / NPV, j = e % NPV;
     sD[e] = (i < n && j < n) ? (S)(P[SL.ad + i * n + j] - (i == j ? 1.0 : 0.0)) : S(0);
@@ -211,7 +224,6 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   const bool prof_on = A.dbg != nullptr && inst == 0 && tid == 0;
   auto score = [&](const S* U) -> S { return small_score<S, NPV>(U, sh, m, p, T, A.r_diag, prof_on ? sprof : nullptr); };
 
-  const RunParams rp = *A.run;
   const uint32_t key0 = (uint32_t)rp.seed, key1 = (uint32_t)(rp.seed >> 32);
   // ---- generation 0: init (Philox / injected) or the resident population (re-score)
   for (int e = tid; e < N * pm; e += nthr) {
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
     if (A.mode == kInitInject) {
       v = A.inj_init[((size_t)inst * N + c) * pm + g];
     } else if (A.mode == kScore || A.mode == kSmallResident) {
-      v = A.pop_io[((size_t)inst * N + c) * pm + g];
+      v = A.pop_in[((size_t)inst * N + c) * pm + g];
     } else {
       // the rollout kernel's init stream: counter (q, cand, instance, "INIT"),
       // genes 2q / 2q + 1 from words (x, y) / (z, w) (K/empc.py:170)
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
   }
   __syncthreads();
   for (int c = tid; c < N; c += nthr)
-    costA[c] = A.mode == kSmallResident ? A.cost_io[(size_t)inst * N + c] : score(popA + (size_t)c * pm);
+    costA[c] = A.mode == kSmallResident ? A.cost_in[(size_t)inst * N + c] : score(popA + (size_t)c * pm);
   __syncthreads();
   int sub = 1;
   while (sub < 32 && N * sub * 2 <= nthr) sub <<= 1;

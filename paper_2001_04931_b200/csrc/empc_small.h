@@ -24,8 +24,13 @@ struct SmallArgs {
   const int* seg;
   const S* cw;
   const S* G;
-  S* pop_io;     // instances x N x pm: read when mode == kScore, final population out
+  const S* pop_in;   // instances x N x pm: read when mode == kScore / kSmallResident
+  const S* cost_in;  // instances x N: read when mode == kSmallResident
+  S* pop_io;     // instances x N x pm: final population out (may be the caller's output slot)
   S* cost_io;    // instances x N
+  // prob / state / run / out may point at mapped pinned host memory (the
+  // public-API graph): the kernel copies the staging blocks into shared
+  // memory once and writes the result block once
   double* out;   // instances x [u (m) | best (pm) | cost | index]
   const S* inj_init;
   // evolves x instances x (N-K) x {2 | pm} (NULL: in-kernel Philox)
