@@ -847,6 +847,22 @@ class Engine final : public EngineBase {
     P.qlist = qlist_;
     P.elite = elite_;
     P.out = out_d_;
+    if (io_out_direct_) {
+      // public-API graph: CTA 0 stores the result into mapped pinned memory,
+      // and the output slot stands in for the ping-pong buffer that ends up
+      // holding the final population (index evolves & 1) -- unless a warm
+      // start still has to read its input from that buffer
+      P.out = out_hd_;
+      io_result_done_ = true;
+      const int fin = r.evolves & 1;
+      if (slot_captured(r) && (r.init || fin == 1)) {
+        Slot& so = slot(r.slot_out);
+        P.pop[fin] = so.cands;
+        P.cost[fin] = so.costs;
+        if (fin == 0) { a.pop_out = so.cands; a.cost_out = so.costs; }
+        io_slot_done_ = true;
+      }
+    }
     {  // helper warps (WS variants) draw the next generation during the recursion
       const int hstart = ((v.ks == 1 ? 1 : 2) * NRG * (tileP / v.CC) + 31) / 32 * 32;
       P.predraw = (v.ws && threads > hstart && !inj && predraw_ok_) ? 1 : 0;
@@ -912,9 +928,11 @@ class Engine final : public EngineBase {
       // straight into the output slot (captured slots; others are copied
       // from pop_[0] after the graph)
       A.prob = stage_prob_hd_; A.state = stage_state_hd_; A.run = run_hd_; A.out = out_hd_;
+      io_result_done_ = true;
       if (slot_captured(r)) {
         Slot& so = slot(r.slot_out);
         A.pop_io = so.cands; A.cost_io = so.costs;
+        io_slot_done_ = true;
       }
     }
     A.mode = r.init ? kInitPhilox : (r.rescore ? kScore : kSmallResident);
@@ -1064,11 +1082,15 @@ class Engine final : public EngineBase {
   }
 
   // result download + copy of the final population into the output slot
-  void enqueue_outputs(int cur, const Slot* so) {
+  void enqueue_outputs(int cur, const Slot* so, bool result = true) {
     const size_t out_bytes = sizeof(double) * (size_t)I_ * out_stride_;
     CopySpans c;
-    if (out_bytes <= kZeroCopyMax) c.add(out_d_, out_hd_, out_bytes);
-    else CK(cudaMemcpyAsync(out_h_, out_d_, out_bytes, cudaMemcpyDeviceToHost, stream_));
+    if (!result) {
+    } else if (out_bytes <= kZeroCopyMax) {
+      c.add(out_d_, out_hd_, out_bytes);
+    } else {
+      CK(cudaMemcpyAsync(out_h_, out_d_, out_bytes, cudaMemcpyDeviceToHost, stream_));
+    }
     if (so != nullptr) {
       c.add(pop_[cur], so->cands, sizeof(S) * (size_t)I_ * d_.N * d_.pm);
       c.add(cost_[cur], so->costs, sizeof(S) * (size_t)I_ * d_.N);
@@ -1104,11 +1126,14 @@ class Engine final : public EngineBase {
       const bool direct = io && small_eligible();
       if (io && !direct) enqueue_h2d();
       io_direct_ = direct;
+      io_out_direct_ = io;
+      io_result_done_ = io_slot_done_ = false;
       cur = enqueue_core(r, nullptr);
-      io_direct_ = false;
-      if (io && !direct) enqueue_outputs(cur, slot_captured(r) ? &slot(r.slot_out) : nullptr);
+      io_direct_ = io_out_direct_ = false;
+      if (io)
+        enqueue_outputs(cur, (slot_captured(r) && !io_slot_done_) ? &slot(r.slot_out) : nullptr, !io_result_done_);
     } catch (...) {
-      io_direct_ = false;
+      io_direct_ = io_out_direct_ = false;
       cudaStreamEndCapture(stream_, &g);
       throw;
     }
@@ -1608,6 +1633,8 @@ class Engine final : public EngineBase {
   double *stage_prob_hd_ = nullptr, *stage_state_hd_ = nullptr, *out_hd_ = nullptr;  // device views of pinned memory
   RunParams* run_hd_ = nullptr;
   bool io_direct_ = false;  // the small solve moves the public-API graph's inputs / outputs itself
+  bool io_out_direct_ = false;                          // capture of a public-API graph: paths may write outputs
+  bool io_result_done_ = false, io_slot_done_ = false;  // ... and report which they wrote
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
   unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key
