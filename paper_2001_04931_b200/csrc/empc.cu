@@ -475,9 +475,9 @@ class Engine final : public EngineBase {
   }
   void pop_free(int id) override {
     Slot& s = slot(id);
-    // graphs that copy into this slot hold its old address
+    // graphs that read or write this slot hold its old address
     for (auto it = graphs_.begin(); it != graphs_.end();) {
-      if (std::get<7>(it->first) == 2 + id) {
+      if (io_code_uses_slot(std::get<7>(it->first), id)) {
         cudaGraphExecDestroy(it->second);
         it = graphs_.erase(it);
       } else {
@@ -823,7 +823,10 @@ class Engine final : public EngineBase {
     a.prob = stage_prob_d_; a.state = stage_state_d_;
     a.idx1 = idx1_; a.idx2 = idx2_; a.seg = seg_; a.cw = cw_; a.G = G_;
     a.stagger = stagger_;
-    a.pop_in = pop_[0]; a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
+    // (a warm graph re-scores straight from the input slot; kScore then also
+    // writes the candidates into pop_out)
+    a.pop_in = warm_src_ ? warm_src_->cands : pop_[0];
+    a.cost_in = nullptr; a.pop_out = pop_[0]; a.cost_out = cost_[0];
     a.elite_idx = elite_; a.run = run_d_;
     a.qcount = nullptr; a.qlist = qlist_; a.qcap = qcap_; a.dbg = nullptr;
     if (phases_ && (size_t)grid * 16 + 32 <= dbg_n_) {
@@ -851,11 +854,12 @@ class Engine final : public EngineBase {
       // public-API graph: CTA 0 stores the result into mapped pinned memory,
       // and the output slot stands in for the ping-pong buffer that ends up
       // holding the final population (index evolves & 1) -- unless a warm
-      // start still has to read its input from that buffer
+      // start still has to read its input from that buffer (a warm graph
+      // reads it from the input slot instead)
       P.out = out_hd_;
       io_result_done_ = true;
       const int fin = r.evolves & 1;
-      if (slot_captured(r) && (r.init || fin == 1)) {
+      if (slot_captured(r) && (r.init || fin == 1 || warm_src_ != nullptr)) {
         Slot& so = slot(r.slot_out);
         P.pop[fin] = so.cands;
         P.cost[fin] = so.costs;
@@ -920,7 +924,8 @@ class Engine final : public EngineBase {
     A.d = d_; A.SL = SL_; A.evolves = r.evolves; A.r_diag = r_diag_ ? 1 : 0;
     A.prob = stage_prob_d_; A.state = stage_state_d_; A.run = run_d_;
     A.idx1 = idx1_; A.idx2 = idx2_; A.seg = seg_; A.cw = cw_; A.G = G_;
-    A.pop_in = pop_[0]; A.cost_in = cost_[0];
+    A.pop_in = warm_src_ ? warm_src_->cands : pop_[0];
+    A.cost_in = warm_src_ ? warm_src_->costs : cost_[0];
     A.pop_io = pop_[0]; A.cost_io = cost_[0]; A.out = out_d_;
     if (io_direct_) {
       // public-API graph: staging read from the mapped pinned buffers, the
@@ -986,6 +991,12 @@ class Engine final : public EngineBase {
       path_desc_ = persist_desc_;
       return r.evolves & 1;
     }
+    if (warm_src_ != nullptr) {  // per-generation launches work on pop_[0]
+      CopySpans c;
+      c.add(warm_src_->cands, pop_[0], sizeof(S) * (size_t)I_ * d_.N * d_.pm);
+      c.add(warm_src_->costs, cost_[0], sizeof(S) * (size_t)I_ * d_.N);
+      launch_copies(c);
+    }
     if (scorer_ == 1 && (r.init || r.rescore || r.evolves > 0)) launch_cond_build();
     if (r.init) {
       const S* inj_init = inj ? (const S*)(*inj)[0] : nullptr;
@@ -1030,7 +1041,7 @@ class Engine final : public EngineBase {
 
   // host staging of a run; `copies` = false leaves the H2D copies to the
   // captured graph (graph_for(r, true))
-  void stage_run(const empc_run_args& r, bool copies = true) {
+  void stage_run(const empc_run_args& r, bool copies = true, bool warm_copy = true) {
     if (!have_sched_) throw InvalidArg{"schedule not set"};
     if (!have_prob_) throw InvalidArg{"problem not set"};
     if (!r.x0 || !r.sigma) throw InvalidArg{"x0 and sigma are required"};
@@ -1049,7 +1060,7 @@ class Engine final : public EngineBase {
     run_h_->thr_cross = (uint64_t)std::llround(std::ldexp(r.crossover_prob, 32));
     run_h_->thr_mut = (uint64_t)std::llround(std::ldexp(r.mutation_prob, 32));
     if (copies) enqueue_h2d();
-    if (!r.init) {
+    if (!r.init && warm_copy) {
       Slot& s = slot(r.slot_in);
       CopySpans c;
       c.add(s.cands, pop_[0], sizeof(S) * (size_t)I_ * d_.N * d_.pm);
@@ -1103,8 +1114,24 @@ class Engine final : public EngineBase {
   // (captured for the first kCapturedSlots slot ids, eager otherwise)
   static constexpr int kCapturedSlots = 4;
   static bool slot_captured(const empc_run_args& r) { return r.slot_out >= 0 && r.slot_out < kCapturedSlots; }
+  // warm public-API runs read their input population straight from a
+  // captured slot_in (no copy before the graph)
+  static bool warm_in_graph(const empc_run_args& r) {
+    return r.init == 0 && r.inject == nullptr && r.slot_in >= 0 && r.slot_in < kCapturedSlots;
+  }
+  // io code of a graph: 0 = no io, else 1 + 8 * (slot_in code) + (slot_out code),
+  // slot codes 0 = not captured, 1 + id otherwise
+  static int io_code_of(const empc_run_args& r, bool io) {
+    if (!io) return 0;
+    const int so = slot_captured(r) ? 1 + r.slot_out : 0;
+    const int si = warm_in_graph(r) ? 1 + r.slot_in : 0;
+    return 1 + 8 * si + so;
+  }
+  static bool io_code_uses_slot(int code, int id) {
+    return code > 0 && (((code - 1) & 7) == 1 + id || ((code - 1) >> 3) == 1 + id);
+  }
   GKey gkey(const empc_run_args& r, bool io) const {
-    const int io_code = !io ? 0 : (slot_captured(r) ? 2 + r.slot_out : 1);
+    const int io_code = io_code_of(r, io);
     return std::make_tuple(r.init != 0, r.rescore != 0, r.evolves, forced_, r_diag_, cps_, scorer_, io_code, tc_mode_,
                            halfk_, persist_mode_ + 4 * persist_tile_ + (small_mode_ + 1) * (1 << 24), halfk_ok_,
                            (incremental_ ? 1 : 0) | (use_radix_ ? 2 : 0) | (radix_persist_ok_ ? 4 : 0));
@@ -1128,12 +1155,15 @@ class Engine final : public EngineBase {
       io_direct_ = direct;
       io_out_direct_ = io;
       io_result_done_ = io_slot_done_ = false;
+      warm_src_ = (io && warm_in_graph(r)) ? &slot(r.slot_in) : nullptr;
       cur = enqueue_core(r, nullptr);
       io_direct_ = io_out_direct_ = false;
+      warm_src_ = nullptr;
       if (io)
         enqueue_outputs(cur, (slot_captured(r) && !io_slot_done_) ? &slot(r.slot_out) : nullptr, !io_result_done_);
     } catch (...) {
       io_direct_ = io_out_direct_ = false;
+      warm_src_ = nullptr;
       cudaStreamEndCapture(stream_, &g);
       throw;
     }
@@ -1150,7 +1180,7 @@ class Engine final : public EngineBase {
   }
 
   void run(const empc_run_args& r) override {
-    stage_run(r, r.inject != nullptr);
+    stage_run(r, r.inject != nullptr, !warm_in_graph(r));
     int cur;
     std::vector<S> init_cast;
     if (r.inject) {
@@ -1635,6 +1665,7 @@ class Engine final : public EngineBase {
   bool io_direct_ = false;  // the small solve moves the public-API graph's inputs / outputs itself
   bool io_out_direct_ = false;                          // capture of a public-API graph: paths may write outputs
   bool io_result_done_ = false, io_slot_done_ = false;  // ... and report which they wrote
+  const Slot* warm_src_ = nullptr;  // capture of a warm public-API graph: the input population's slot
   int out_stride_ = 0;
   int *idx1_ = nullptr, *idx2_ = nullptr, *seg_ = nullptr;
   unsigned long long* amin_d_ = nullptr;  // persistent solve: argmin key

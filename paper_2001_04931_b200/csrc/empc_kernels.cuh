@@ -350,7 +350,7 @@ __device__ __forceinline__ bool breed_tile(const RolloutArgs<S>& a, int inst, in
         const S lo = cumin[l], hi = cumax[l];
         v = v < lo ? lo : (v > hi ? hi : v);
       }
-      if (a.mode != kScore) a.pop_out[(pop_base + a.row0 + cand) * pm + g] = v;
+      if (a.mode != kScore || a.pop_in != a.pop_out) a.pop_out[(pop_base + a.row0 + cand) * pm + g] = v;
     }
     UsT[g * tPS + c] = v;
   }

@@ -80,3 +80,45 @@ def test_random_shapes_every_path(shape, path):
         assert "resident single-CTA" in desc, desc
     if path == "launches":
         assert "per-generation" in desc, desc
+
+
+WARM_SHAPES = [SHAPES[1], SHAPES[4], SHAPES[6]]
+
+
+@pytest.mark.parametrize("shape", WARM_SHAPES, ids=[f"n{s[0]}_N{s[4]}" for s in WARM_SHAPES])
+@pytest.mark.parametrize("path", sorted(PATHS))
+def test_warm_start_reads_the_input_population_in_place(shape, path):
+    """Warm public-API solves read `prev` straight from its slot inside the
+    graph (no copy before it): `prev` stays untouched, the result is the
+    oracle-consistent re-score + G generations, and repeating the call with
+    the same `prev` gives the same bits (both slot alternations)."""
+    n, m, T, p, N, K, G, dense_r = shape
+    rng = np.random.default_rng(17 + n)
+    spec, x0 = _random_problem(rng, n, m, T, dense_r)
+    sched = P.KnotSchedule(T, p)
+    st = P.EmpcSettings(num_sims=N, num_parents=K, generations=G, seed=4)
+    ctx = E._spec_context(spec, sched, st)
+    pr = O.Problem.from_spec(spec)
+    try:
+        for opt, val in PATHS[path].items():
+            ctx.h.set_option(opt, val)
+        cold = P.solve_empc(spec, sched, st, x0)
+        prev = cold.population
+        before = (prev.candidates.copy(), prev.costs.copy())
+        x1 = x0 + 0.05
+        runs = [P.solve_empc(spec, sched, st, x1, prev) for _ in range(3)]
+        desc = ctx.h.describe()
+    finally:
+        for opt, val in RESET.items():
+            ctx.h.set_option(opt, val)
+    np.testing.assert_array_equal(prev.candidates, before[0])
+    np.testing.assert_array_equal(prev.costs, before[1])
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r.population.candidates, runs[0].population.candidates)
+        np.testing.assert_array_equal(r.population.costs, runs[0].population.costs)
+        assert r.best_cost == runs[0].best_cost
+    c, k = runs[0].population.candidates, runs[0].population.costs
+    np.testing.assert_allclose(k, O.rollout_costs(c, pr, x1), rtol=1e-5, err_msg=desc)
+    assert np.all(np.diff(k[:K]) >= 0), desc
+    assert runs[0].best_cost == np.min(k)
+    assert runs[0].population.generation == prev.generation + G
