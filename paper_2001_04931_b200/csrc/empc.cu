@@ -30,7 +30,7 @@
 
 using namespace empc;
 
-namespace {
+namespace empc {
 
 // Byte-range copies by one kernel (16-byte words when a range allows it).
 // The public-API graph moves its inputs and outputs with these instead of
@@ -75,6 +75,9 @@ __global__ void copy_spans_kernel(const CopySpans c) {
 }
 // host-memory spans above this size stay DMA copies (C5 stages 110 MB)
 constexpr size_t kZeroCopyMax = (size_t)1 << 20;
+}  // namespace empc
+
+namespace {
 
 thread_local std::string g_create_error;
 
