@@ -1033,7 +1033,7 @@ class Engine final : public EngineBase {
       post();
       cur ^= 1;
     }
-    launch_ex(finalize_kernel<S>, dim3(I_), dim3(256), 0, pdl_next_, (const S*)pop_[cur], (const S*)cost_[cur], d_.N,
+    launch_ex(finalize_kernel<S>, dim3(I_), dim3(I_ == 1 ? 1024 : 256), 0, pdl_next_, (const S*)pop_[cur], (const S*)cost_[cur], d_.N,
               d_.m, d_.pm, out_d_);
     pdl_next_ = false;
     ++launches_;

@@ -1506,12 +1506,24 @@ __device__ __forceinline__ void finalize_body(const S* __restrict__ cands, const
   pdl_wait();
   uint64_t bo = ~0ull;
   int bi = 0x7FFFFFFF;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const S v = c[i];
-    uint64_t o;
-    if constexpr (sizeof(S) == 4) o = (v != v) ? 0ull : (uint64_t)ord32((float)v);
-    else o = (v != v) ? 0ull : ord64((double)v);
-    if (o < bo || (o == bo && i < bi)) { bo = o; bi = i; }
+  // four independent loads in flight per thread (C4: 16k costs, one CTA)
+  for (int i0 = threadIdx.x; i0 < N; i0 += 4 * blockDim.x) {
+    S v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < N ? c[i] : S(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < N) {
+        uint64_t o;
+        if constexpr (sizeof(S) == 4) o = (v[u] != v[u]) ? 0ull : (uint64_t)ord32((float)v[u]);
+        else o = (v[u] != v[u]) ? 0ull : ord64((double)v[u]);
+        if (o < bo || (o == bo && i < bi)) { bo = o; bi = i; }
+      }
+    }
   }
   for (int off = 16; off > 0; off >>= 1) {
     const uint64_t o2 = __shfl_down_sync(0xFFFFFFFFu, bo, off);
