@@ -130,7 +130,12 @@ typedef struct {
 } empc_run_args;
 
 /* Run init / rescore / evolves as one device-resident sequence (graph-captured
- * when no injection is given).  Synchronous: returns after outputs are on the host. */
+ * when no injection is given).  Synchronous: returns after outputs are on the host.
+ * Inside the graph the inputs (x0, sigma, run parameters and the problem
+ * staging, <= 1 MB) are read from the handle's mapped pinned buffers by
+ * kernels, the result block is stored into mapped pinned memory, and the
+ * final population goes into slot_out (ids < 4 captured, others copied after);
+ * a warm start reads slot_in in place and leaves it unchanged. */
 int empc_run(empc_handle* h, const empc_run_args* args);
 
 /* Score `num` candidates per instance at x0 (instances x n) with the rollout
