@@ -1678,7 +1678,7 @@ class Engine final : public EngineBase {
   // tests pass in that mode) but measured slower at C3 (34.5 vs 31.3 us per
   // generation), so opt-in
   bool one_sync_ok_ = std::getenv("EMPC_ONE_SYNC") != nullptr;
-  int ws_threads_ = 352;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)
+  int ws_threads_ = 384;  // threads of a warp-synchronous persistent CTA (helpers beyond the candidate warps)
   S *cw_ = nullptr, *G_ = nullptr;
   double *W64_ = nullptr, *G64_ = nullptr;  // FP64 W (T x p) and W'W for the condensed build
   int scorer_ = 0;
