@@ -713,12 +713,16 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
   // own CH candidates first (base XO) and its partner's second (base XP), so
   // folding the halves is one shuffle + one add per result, no selects.
   // A macro, not a lambda, so the register arrays stay in registers.
-#define EMPC_MATVEC(FROMREG, MS, XO, XP, OUT)                                                         \
+#define EMPC_MATVEC(FROMREG, MS, XO, XP, OUT, SEEDED, SEED)                                           \
   {                                                                                                   \
     S part_[RR][CC][NSPLIT];                                                                          \
     _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                    \
     _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                    \
     _Pragma("unroll") for (int s = 0; s < NSPLIT; ++s) part_[r][q][s] = S(0);                         \
+    if constexpr (SEEDED) {                                                                           \
+      _Pragma("unroll") for (int r = 0; r < RR; ++r)                                                  \
+      _Pragma("unroll") for (int q = 0; q < CH; ++q) part_[r][q][0] = (SEED)[r][q];                   \
+    }                                                                                                 \
     S xv_[2][CC][VEC];                                                                                \
     _Pragma("unroll") for (int q = 0; q < CC; ++q)                                                    \
       lds_vec<S, VEC>((q < CH ? (XO) + q * NPS : (XP) + (q - CH) * NPS), xv_[0][q]);                 \
@@ -795,6 +799,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     }
   }
   int rdo = 0, wro = bufstride;
+  constexpr bool kSeedStep = sizeof(S) == 4;
   for (int k0 = 0; run_loop && k0 < T;) {
     const int k1 = sSeg[k0];
     const int i1 = sI1[k0], i2 = sI2[k0];
@@ -808,18 +813,28 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
       for (int q = 0; q < CH; ++q) db[r][q] = t2[q] - b1[r][q];
     }
     for (int k = k0; k < k1; ++k) {
-      S ax[RR][CH];
-      EMPC_MATVEC(AREG, As, xo0 + rdo, xp0 + rdo, ax)
-      S qx[DQ ? RR : 1][DQ ? CH : 1];
-      if constexpr (DQ) EMPC_MATVEC(false, Qs, xo0 + rdo, xp0 + rdo, qx)
       const S ck = sC[k];
+      // FP32: the step's e + drive seeds this lane's own accumulators, so
+      // it is computed off the critical path and the folded matvec is the
+      // next state (FP64 keeps the reference-order update below)
+      S xd[RR][CH];
+      if constexpr (kSeedStep) {
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int q = 0; q < CH; ++q) xd[r][q] = xo[r][q] + fma(ck, db[r][q], b1[r][q]);
+      }
+      S ax[RR][CH];
+      EMPC_MATVEC(AREG, As, xo0 + rdo, xp0 + rdo, ax, kSeedStep, xd)
+      S qx[DQ ? RR : 1][DQ ? CH : 1];
+      if constexpr (DQ) EMPC_MATVEC(false, Qs, xo0 + rdo, xp0 + rdo, qx, false, xd)
       S* xw = xw0 + wro;
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           if constexpr (DQ) cst[q] = fma(xo[r][q], qx[r][q], cst[q]);  // e_k' Q e_k
-          const S en = xo[r][q] + fma(ck, db[r][q], ax[r][q] + b1[r][q]);
+          const S en = kSeedStep ? ax[r][q] : xo[r][q] + fma(ck, db[r][q], ax[r][q] + b1[r][q]);
           xo[r][q] = en;
           if constexpr (!DQ) srow[r][q] = fma(en, en, srow[r][q]);  // e_{k+1,i}^2
 #ifndef EMPC_EXP_NOSTS
@@ -850,7 +865,7 @@ __device__ __forceinline__ void rollout_body(const RolloutArgs<S>& a, bool stage
     // terminal state term e_T' Q e_T
     const int rd = (T & 1) ? bufstride : 0;
     S qf[RR][CH];
-    EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qf)
+    EMPC_MATVEC(false, Qs, xo0 + rd, xp0 + rd, qf, false, qf)
 #pragma unroll
     for (int r = 0; r < RR; ++r)
 #pragma unroll
