@@ -1007,8 +1007,14 @@ __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, 
   pdl_trigger();  // the next rollout may start its independent prologue
   const int M = full ? N : K + L;
   const OT* ql = full ? nullptr : reinterpret_cast<const OT*>(qlist_in) + (size_t)inst * qcap * 2;
+  // FP32: one 64-bit key (ord << 32 | row) per candidate, so a comparison is
+  // a single unsigned compare (same order as (ord, row) pairs)
+  unsigned long long* kk = reinterpret_cast<unsigned long long*>(smem_raw);
   for (int j = tid; j < M; j += nthr) {
-    if (j < K || full) {
+    if constexpr (sizeof(S) == 4) {
+      if (j < K || full) kk[j] = ((unsigned long long)ord32((float)__ldcg(c + j)) << 32) | (unsigned)j;
+      else kk[j] = ((unsigned long long)__ldcg(ql + 2 * (j - K)) << 32) | (unsigned)__ldcg(ql + 2 * (j - K) + 1);
+    } else if (j < K || full) {
       ck[j] = OrdOf<S>::ord(c[j]);
       ci[j] = j;
     } else {
@@ -1020,12 +1026,18 @@ __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, 
   const int per = (M + gridDim.x - 1) / gridDim.x;
   const int e0 = blockIdx.x * per, e1 = min(M, e0 + per);
   for (int e = e0 + warp; e < e1; e += nwarps) {
-    const OT ke = ck[e];
-    const int re = ci[e];
-    int cnt = 0;
-    for (int j = lane; j < M; j += 32) {
-      const OT kj = ck[j];
-      cnt += (kj < ke || (kj == ke && ci[j] < re)) ? 1 : 0;
+    int re, cnt = 0;
+    if constexpr (sizeof(S) == 4) {
+      const unsigned long long ke = kk[e];
+      re = (int)(uint32_t)ke;
+      for (int j = lane; j < M; j += 32) cnt += kk[j] < ke ? 1 : 0;
+    } else {
+      const OT ke = ck[e];
+      re = ci[e];
+      for (int j = lane; j < M; j += 32) {
+        const OT kj = ck[j];
+        cnt += (kj < ke || (kj == ke && ci[j] < re)) ? 1 : 0;
+      }
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
     if (cnt < K) {
