@@ -269,7 +269,12 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
     S* const cc = cur ? costB : costA;
     S* const cn = cur ? costA : costB;
     // ---- stable selection (K/empc.py:185-188): rank of (ord(cost), row)
-    for (int c = tid; c < N; c += nthr) keys[c] = ord_key(cc[c]);
+    // (FP32: one 64-bit key ord << 32 | row, a single unsigned compare)
+    unsigned long long* const kk = reinterpret_cast<unsigned long long*>(keys);
+    for (int c = tid; c < N; c += nthr) {
+      if constexpr (sizeof(S) == 4) kk[c] = ((unsigned long long)ord_key(cc[c]) << 32) | (unsigned)c;
+      else keys[c] = ord_key(cc[c]);
+    }
     __syncthreads();
     mark(0);
     // `sub` lanes (a power of two <= 32) count the rank of one candidate
@@ -278,10 +283,15 @@ __global__ void __launch_bounds__(512, 1) small_solve_kernel(const SmallArgs<S> 
       const bool valid = c < N;
       int r = 0;
       if (valid) {
-        const OT kc = keys[c];
-        for (int j = part; j < N; j += sub) {
-          const OT kj = keys[j];
-          r += (kj < kc || (kj == kc && j < c)) ? 1 : 0;
+        if constexpr (sizeof(S) == 4) {
+          const unsigned long long kc = kk[c];
+          for (int j = part; j < N; j += sub) r += kk[j] < kc ? 1 : 0;
+        } else {
+          const OT kc = keys[c];
+          for (int j = part; j < N; j += sub) {
+            const OT kj = keys[j];
+            r += (kj < kc || (kj == kc && j < c)) ? 1 : 0;
+          }
         }
       }
       for (int o = 1; o < sub; o <<= 1) r += __shfl_xor_sync(0xFFFFFFFFu, r, o);
