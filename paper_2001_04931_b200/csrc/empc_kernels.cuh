@@ -981,7 +981,10 @@ __host__ __device__ inline size_t select_smem(int N) {
   return (size_t)N * (sizeof(OT) + sizeof(int));
 }
 
-template <typename S>
+// PF > 0 (FP32): each ranked candidate's row (pm <= 32 PF) and cost are
+// loaded before its rank is known, so the elite carry-over's L2 round trip
+// overlaps the counting (costs PF registers per lane)
+template <typename S, int PF = 0>
 __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, int K, int* __restrict__ elite_idx,
                                             int incremental, int* __restrict__ qcount_in,
                                             const void* __restrict__ qlist_in, int* __restrict__ qcount_next, int qcap,
@@ -1027,9 +1030,23 @@ __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, 
   const int e0 = blockIdx.x * per, e1 = min(M, e0 + per);
   for (int e = e0 + warp; e < e1; e += nwarps) {
     int re, cnt = 0;
+    constexpr int kPF = PF > 0 ? PF : 1;
+    S rowv[kPF];
+    S cre = S(0);
+    bool pf = false;
     if constexpr (sizeof(S) == 4) {
       const unsigned long long ke = kk[e];
       re = (int)(uint32_t)ke;
+      pf = PF > 0 && pop_out != nullptr && pm <= 32 * kPF;
+      if (pf) {
+        const S* from = pop_in + ((size_t)inst * N + re) * pm;
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) {
+          const int g = lane + 32 * i;
+          rowv[i] = g < pm ? __ldcg(from + g) : S(0);
+        }
+        cre = __ldcg(c + re);
+      }
       for (int j = lane; j < M; j += 32) cnt += kk[j] < ke ? 1 : 0;
     } else {
       const OT ke = ck[e];
@@ -1045,10 +1062,19 @@ __device__ __forceinline__ void select_body(const S* __restrict__ costs, int N, 
       if (pop_out != nullptr) {
         // elite carry-over (K/empc.py:186-188, 206): rows [0, K) of the next
         // population are the sorted elites with their carried costs
-        const S* from = pop_in + ((size_t)inst * N + re) * pm;
         S* to = pop_out + ((size_t)inst * N + cnt) * pm;
-        for (int g = lane; g < pm; g += 32) to[g] = from[g];
-        if (lane == 0) cost_out[(size_t)inst * N + cnt] = c[re];
+        if (pf) {
+#pragma unroll
+          for (int i = 0; i < kPF; ++i) {
+            const int g = lane + 32 * i;
+            if (g < pm) to[g] = rowv[i];
+          }
+          if (lane == 0) cost_out[(size_t)inst * N + cnt] = cre;
+        } else {
+          const S* from = pop_in + ((size_t)inst * N + re) * pm;
+          for (int g = lane; g < pm; g += 32) to[g] = from[g];
+          if (lane == 0) cost_out[(size_t)inst * N + cnt] = c[re];
+        }
       }
     }
   }
@@ -1771,12 +1797,12 @@ __global__ void __launch_bounds__(MAXT, 1) persist_kernel(const PersistArgs<S> P
                              P.pop[cur], P.pop[cur ^ 1], P.cost[cur ^ 1], pm, nullptr, nullptr,
                              gt != nullptr ? gt + 32 : nullptr);
       } else {
-        select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+        select_body<S, (NP >= 24 ? 8 : 0)>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
                        (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
                        P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
       }
     } else {
-      select_body<S>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
+      select_body<S, (NP >= 24 ? 8 : 0)>(P.cost[cur], N, K, P.elite, inc, inc ? P.qcount + ((g - 1) & 1) : nullptr,
                      (const char*)P.qlist + ((g - 1) & 1) * qstride, P.qcount + (g & 1), a.qcap, P.pop[cur],
                      P.pop[cur ^ 1], P.cost[cur ^ 1], pm);
     }
